@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""SageAttn-B forward throughput on B200 (paper OPS = 4*B*H*N^2*d / t, halved for causal).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl ours|reference]
+
+One step = the whole hot path on one batch of synthetic fp16 inputs already
+resident in HBM: K1 (smooth-K + INT8 quantization, 2 launches) + K2 (tcgen05
+attention, 1 launch).  Under torchrun (N>1) the B*H units are head-sharded
+over the ranks (K3, no collective on the data path); time = max over ranks.
+
+Default workload = BASELINE.json configs[1] (C2, Llama-2-7B prefill:
+B=1, H=32, N=8192, d=128, causal).  Other workloads (C1, C3, C4-<d>-<N>-<c|nc>,
+C5) are selectable with --workload.
+
+Keys beyond the driver contract:
+  e2e          same metric through the C-ABI host-buffer call (sab_attention_fwd_host)
+               with pinned host fp16 inputs; H2D of Q/K/V and D2H of O inside the timed region
+  roofline     K2 (dominant kernel): paper-OPS / K2 time vs the mixed INT8+FP16 tensor peak
+  roofline_k1  K1: algorithmic bytes / K1 time vs measured HBM copy bandwidth
+  cpu_baseline the reference's own CPU code (oracle/_ref) on a bounded sample, rank 0 only
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "C1": dict(batch=1, heads=2, tokens=1024, head_dim=64, causal=False, name="C1 oracle case (1,2,1024,64) non-causal"),
+    "C2": dict(batch=1, heads=32, tokens=8192, head_dim=128, causal=True,
+               name="C2 Llama-2-7B prefill attention (1,32,8192,128) causal"),
+    "C3": dict(batch=2, heads=30, tokens=17776, head_dim=64, causal=False,
+               name="C3 CogVideoX-2B attention (2,30,17776,64) non-causal"),
+    "C5": dict(batch=1, heads=64, tokens=131072, head_dim=128, causal=True,
+               name="C5 long-context prefill (1,64,131072,128) causal"),
+}
+METRIC = "attention TOPS (4*B*H*N^2*d/s, halved for causal), SageAttn-B forward (K1 prepass + K2 attention)"
+UNIT = "TOPS"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def workload(name: str):
+    if name in WORKLOADS:
+        return dict(WORKLOADS[name])
+    if name.startswith("C4-"):  # C4-<d>-<N>-<c|nc>
+        _, d, n, c = name.split("-")
+        return dict(batch=4, heads=32, tokens=int(n), head_dim=int(d), causal=(c == "c"),
+                    name=f"C4 kernel-bench point (4,32,{n},{d}) {'causal' if c == 'c' else 'non-causal'}")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def paper_ops(units: int, n: int, d: int, causal: bool) -> float:
+    ops = 4.0 * units * n * n * d
+    return ops / 2 if causal else ops
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """NVML sampler (every 20 ms) of SM clock and throttle reasons while the GPU is busy."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                if util > 0:
+                    self.samples.append(mhz)
+                    for bit, name in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU reference sample
+
+def sample_tiles(n: int, causal: bool, n_tiles: int):
+    ntq = -(-n // 128)
+    n_tiles = max(1, min(n_tiles, ntq))
+    return sorted({int(round(i * (ntq - 1) / max(1, n_tiles - 1))) for i in range(n_tiles)}) if n_tiles > 1 else [ntq // 2]
+
+
+def tile_ops(n: int, d: int, causal: bool, tiles):
+    """Paper-OPS of the sampled query tiles: 4*d per (query, attended key) pair."""
+    total = 0
+    for t in tiles:
+        r0, r1 = t * 128, min(n, t * 128 + 128)
+        keys = sum(r + 1 for r in range(r0, r1)) if causal else (r1 - r0) * n
+        total += 4 * keys * d
+    return float(total)
+
+
+def cpu_reference_sample(wl, threads: int, target_s: float = 12.0):
+    """Runs the reference's own CPU code (oracle/_ref, kind "reference") on query tiles of unit 0.
+
+    Returns (TOPS, seconds, description, threads, kind)."""
+    import numpy as np
+
+    from paper_2410_02367_b200 import synth
+
+    n, d, causal = wl["tokens"], wl["head_dim"], wl["causal"]
+    q, k, v = (x[0] for x in synth.qkv(1, n, d, dtype=np.float32))
+    kind = "reference"
+    try:
+        from oracle.oracle import Reference
+
+        ref = Reference()
+    except (FileNotFoundError, OSError):
+        ref, kind = None, "port"
+    # ~0.3 GOPS per core: size the sample so one round takes ~target_s of wall time.
+    per_tile = tile_ops(n, d, causal, [(-(-n // 128)) // 2]) / 0.3e9
+    per_thread = max(1, int(target_s / max(per_tile, 1e-3)))
+    tiles_all = sample_tiles(n, causal, threads * per_thread)
+    lists = [tiles_all[i::threads] for i in range(threads) if tiles_all[i::threads]]
+    t0 = time.perf_counter()
+    if ref is not None:
+        ref.sage_b_tiles_parallel(q, k, v, lists, causal)
+    else:
+        from oracle.oracle import Oracle
+
+        orc = Oracle()
+        pre = orc.prepass(q[None], k[None])
+        ths = [threading.Thread(target=orc.sage_b_tiles, args=(pre, v[None], 0, tl, causal, False)) for tl in lists]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    dt = time.perf_counter() - t0
+    ops = tile_ops(n, d, causal, tiles_all)
+    desc = (f"{len(tiles_all)} of {-(-n // 128)} query tiles (128 rows each) of unit 0 of {wl['name']}, "
+            f"SageAttn-B default FP16-accumulator arm, {len(lists)} host threads, {ops:.3e} paper-OPS")
+    return ops / dt / 1e12, dt, desc, len(lists), kind
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=None)
+    args = ap.parse_args()
+    wl = workload(args.workload)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    units_total = wl["batch"] * wl["heads"]
+    n, d, causal = wl["tokens"], wl["head_dim"], wl["causal"]
+    total_ops = paper_ops(units_total, n, d, causal)
+    config = {"workload": wl["name"], "batch": wl["batch"], "heads": wl["heads"], "tokens": n, "head_dim": d,
+              "causal": causal, "parallelism": f"head-shard x{world}" if world > 1 else "single GPU",
+              "l2": "inputs (3 x fp16 Q/K/V) larger than L2, and L2 flushed between timed steps"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = args.cpu_threads or os.cpu_count() or 1
+        for _ in range(args.warmup):
+            cpu_reference_sample(wl, threads, target_s=1.0)
+        vals, secs = [], []
+        desc = kind = None
+        for _ in range(args.steps):
+            v, s, desc, used, kind = cpu_reference_sample(wl, threads, target_s=1.0)
+            vals.append(v)
+            secs.append(s)
+        value = statistics.median(vals)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int8 QK / fp16 PV (binary16 emulated on CPU)",
+                "data": "synthetic N(0,1) fp16 (seeded counter RNG), widened to fp32 for the reference",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind, "sample": desc},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_2410_02367_b200 import _lib, sageattn, synth
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    first, count = _lib.shard_plan(units_total, world, rank)
+
+    # Synthetic inputs of this rank's shard (global-index RNG: the shard equals the slice).
+    per_unit = n * d
+    if count * per_unit <= (1 << 28):
+        host = [torch.from_numpy(synth.tensor(s, (count, n, d), first)).reshape(1, count, n, d) for s in (1, 2, 3)]
+        data = "synthetic N(0,1) fp16 from the seeded counter RNG (global index), Q/K/V seeds 1/2/3"
+    else:
+        g = torch.Generator().manual_seed(1234 + first)
+        host = [torch.randn((1, count, n, d), generator=g, dtype=torch.float32).half() for _ in range(3)]
+        data = "synthetic N(0,1) fp16 (torch.randn, seeded per shard)"
+    q, k, v = (h.to(dev) for h in host)
+    o = torch.empty_like(q)
+    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16)
+    ws = sageattn.Workspace(desc, dev)
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    lib = _lib.load()
+    import ctypes as C
+
+    def step():
+        _lib.check(lib.sab_prepass(C.byref(desc), q.data_ptr(), k.data_ptr(), None, ws.ptr, ws.nbytes, sp))
+        ev[1].record(stream)
+        _lib.check(lib.sab_attention(C.byref(desc), ws.ptr, ws.nbytes, v.data_ptr(), o.data_ptr(), sp))
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        ev[0].record(stream)
+        step()
+        ev[2].record(stream)
+    torch.cuda.synchronize()
+    _lib.check(sageattn.read_status(ws))
+
+    sampler = ClockSampler(local_rank)
+    t_step, t_k1, t_k2 = [], [], []
+    with sampler:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(2)  # evict the previous step's data from L2 (outside the timed events)
+            ev[0].record(stream)
+            step()
+            ev[2].record(stream)
+            ev[2].synchronize()
+            t_step.append(ev[0].elapsed_time(ev[2]))
+            t_k1.append(ev[0].elapsed_time(ev[1]))
+            t_k2.append(ev[1].elapsed_time(ev[2]))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+        # ---- end to end through the C-ABI host-buffer call (pinned host fp16 in, fp16 out)
+        e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+        hq, hk, hv = (h.contiguous().pin_memory().numpy() for h in host)
+        ho = torch.empty(hq.shape, dtype=torch.float16).pin_memory().numpy()
+        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[local_rank])  # warm the context pool
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[local_rank])
+        e2e_s = time.perf_counter() - t0
+
+    local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(local, op=dist.ReduceOp.MAX)
+    tot_ms, k1_ms, k2_ms, e2e_max = local.tolist()
+    ms_per_step = tot_ms / args.steps
+    value = total_ops / (ms_per_step * 1e-3) / 1e12
+    e2e_value = total_ops * e2e_steps / e2e_max / 1e12
+
+    # Roofline of K2 (dominant): paper-OPS per launch / mean K2 time on this rank.
+    peaks, peak_src = measured_peaks()
+    p_f16 = peaks["bf16_tflops"]
+    p_mix = 4.0 / (2.0 / (2.0 * p_f16) + 2.0 / p_f16)  # QK on the INT8 pipe (2x fp16 rate), PV on fp16
+    shard_ops = paper_ops(count, n, d, causal)
+    k2_mean_ms = statistics.mean(t_k2)
+    k2_ach = shard_ops / (k2_mean_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
+            tr = json.load(f).get(f"{args.workload}")
+            traffic = tr
+    except (OSError, ValueError):
+        pass
+    k1_bytes = count * (6 * n * d + 4 * (-(-n // 128) + -(-n // 64) + d)) + count * 2 * n * d  # + K re-read
+    k1_alg = count * (6 * n * d + 4 * (-(-n // 128) + -(-n // 64) + d))
+    k1_mean_ms = statistics.mean(t_k1)
+
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8 QK^T (s32 acc) / fp16 PV (fp32 acc); fp16 Q/K/V/O",
+        "data": data, "config": config,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * units_total * n * d * 2,
+                "d2h_bytes_per_step": units_total * n * d * 2,
+                "how": "sab_attention_fwd_host on pinned host buffers, wall clock, max over ranks"},
+        "gpu_launches": args.steps * 3,  # k1_mean_partials + k1_quantize + k2_attention
+        "roofline": {"bound": "tensor", "achieved": k2_ach, "peak": p_mix, "unit": "TFLOP/s",
+                     "frac": k2_ach / p_mix, "traffic": traffic, "kernel": "k2_attention",
+                     "ms_per_launch": k2_mean_ms,
+                     "peak_source": f"{peak_src} bf16_tflops={p_f16} for the fp16 PV half, 2x for the int8 QK half "
+                                    "(datasheet ratio); paper-OPS are int8+fp16 ops",
+                     "frac_of_int8_dense_peak": k2_ach / (2.0 * p_f16)},
+        "roofline_k1": {"bound": "hbm", "achieved": k1_alg / (k1_mean_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                        "unit": "GB/s", "frac": k1_alg / (k1_mean_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                        "ms_per_step": k1_mean_ms, "alg_bytes": k1_alg, "min_dram_bytes_with_k_reread": k1_bytes},
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        threads = args.cpu_threads or os.cpu_count() or 1
+        v_cpu, s_cpu, sdesc, used, kind = cpu_reference_sample(wl, threads)
+        line["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": used, "kind": kind, "sample": sdesc,
+                                "seconds": s_cpu}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,543 @@
+// sab_capi.cu -- the extern "C" boundary (include/sageattn_b200.h).
+//
+// Validation mirrors the reference entry (attention.hpp:320-322, 98-103;
+// tensor.hpp:70-71); launches K1 (sab_prepass.cu) and K2 (sab_attention.cu);
+// the host-buffer entry implements K3, the head x batch partition of
+// attention.hpp:357-358 over 1..8 devices (one host thread per device, no
+// collective: units are independent).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "sab_internal.h"
+
+using namespace sab;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return set_error(SAB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int64_t units_of(const sab_desc* d) { return int64_t(d->batch) * d->heads; }
+
+int elem_size(int dtype) { return dtype == SAB_F32 ? 4 : 2; }
+
+int layout_of(const sab_desc* d, sab_ws_layout* L) {
+    const size_t units = size_t(units_of(d));
+    const size_t n = size_t(d->tokens), hd = size_t(d->head_dim);
+    const int depth = tree_depth(d->tokens);
+    const int npc = nodes_per_cta(depth);
+    const int n_partials = (1 << depth) / npc;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = off;
+        off = align_up(off + bytes, 256);
+        return uint64_t(at);
+    };
+    L->qcodes = take(units * n * hd);
+    L->kcodes = take(units * n * hd);
+    L->qscales = take(units * ((n + kBlockQ - 1) / kBlockQ) * sizeof(float));
+    L->kscales = take(units * ((n + kBlockKV - 1) / kBlockKV) * sizeof(float));
+    L->mean_k = take(units * hd * sizeof(float));
+    L->partials = take(units * size_t(n_partials) * hd * sizeof(float));
+    L->v16 = take(d->in_dtype == SAB_F32 ? units * n * hd * 2 : 0);
+    L->status = take(sizeof(int32_t));
+    L->total = off;
+    L->n_partials = n_partials;
+    L->tree_depth = depth;
+    return SAB_OK;
+}
+
+template <typename T>
+T* at(void* base, uint64_t off) {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(base) + off);
+}
+
+PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const void* q, const void* k, const void* v,
+                             void* ws) {
+    PrepassParams p{};
+    p.q = q;
+    p.k = k;
+    p.v = v;
+    p.qcodes = at<int8_t>(ws, L.qcodes);
+    p.kcodes = at<int8_t>(ws, L.kcodes);
+    p.qscales = at<float>(ws, L.qscales);
+    p.kscales = at<float>(ws, L.kscales);
+    p.mean = at<float>(ws, L.mean_k);
+    p.partials = at<float>(ws, L.partials);
+    p.v16 = d->in_dtype == SAB_F32 ? at<uint16_t>(ws, L.v16) : nullptr;
+    p.status = at<int>(ws, L.status);
+    p.units = int(units_of(d));
+    p.n = d->tokens;
+    p.d = d->head_dim;
+    p.depth = L.tree_depth;
+    p.nodes_per_cta = nodes_per_cta(L.tree_depth);
+    p.n_partials = L.n_partials;
+    p.smooth = d->smooth_k != 0;
+    p.check_v = d->check_v != 0;
+    p.in_f32 = d->in_dtype == SAB_F32;
+    p.inv_n = 1.0f / static_cast<float>(d->tokens);
+    p.fold = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d->head_dim)));
+    return p;
+}
+
+AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws, const void* v, void* o) {
+    AttnParams a{};
+    void* w = const_cast<void*>(ws);
+    a.qcodes = at<int8_t>(w, L.qcodes);
+    a.kcodes = at<int8_t>(w, L.kcodes);
+    a.qscales = at<float>(w, L.qscales);
+    a.kscales = at<float>(w, L.kscales);
+    a.v16 = d->in_dtype == SAB_F32 ? static_cast<const void*>(at<uint16_t>(w, L.v16)) : v;
+    a.o = o;
+    a.status = at<int>(w, L.status);
+    a.units = int(units_of(d));
+    a.n = d->tokens;
+    a.d = d->head_dim;
+    a.causal = d->causal != 0;
+    a.out_f32 = d->out_dtype == SAB_F32;
+    return a;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int enqueue_prepass(const sab_desc* d, const sab_ws_layout& L, const void* q, const void* k, const void* v, void* ws,
+                    cudaStream_t s, bool reset) {
+    if (reset) {
+        cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: status reset");
+    }
+    cudaError_t e = launch_prepass(prepass_params(d, L, q, k, v, ws), s);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: launch");
+    return SAB_OK;
+}
+
+int enqueue_attention(const sab_desc* d, const sab_ws_layout& L, void* ws, const void* v, void* o, cudaStream_t s) {
+    cudaError_t e = launch_attention(attn_params(d, L, ws, v, o), s);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_attention: launch");
+    return SAB_OK;
+}
+
+int map_status_word(int word) {
+    if (word & kStatusNonFinite) return set_error(SAB_ERR_NONFINITE, "sage_attention: non-finite input");
+    if (word & kStatusOverflow)
+        return set_error(SAB_ERR_OVERFLOW, "sage_attention: binary16 P~V accumulator overflowed");
+    return SAB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sab_status_string(int status) {
+    switch (status) {
+        case SAB_OK: return "ok";
+        case SAB_ERR_SHAPE: return "bad shape or block sizes";
+        case SAB_ERR_NONFINITE: return "sage_attention: non-finite input";
+        case SAB_ERR_OVERFLOW: return "sage_attention: binary16 P~V accumulator overflowed";
+        case SAB_ERR_CUDA: return "CUDA error";
+        case SAB_ERR_UNSUPPORTED: return "option outside the SAGEAttn-B B200 path";
+        case SAB_ERR_WORKSPACE: return "workspace missing or too small";
+        case SAB_ERR_NO_DEVICE: return "no sm_100 device";
+        case SAB_ERR_ARGUMENT: return "bad argument";
+        default: return "unknown status";
+    }
+}
+
+const char* sab_last_error(void) { return g_last_error.c_str(); }
+
+int sab_abi_version(void) { return SAB_ABI_VERSION; }
+
+void sab_desc_init(sab_desc* d, int32_t batch, int32_t heads, int32_t tokens, int32_t head_dim, int32_t causal) {
+    if (!d) return;
+    std::memset(d, 0, sizeof(*d));
+    d->batch = batch;
+    d->heads = heads;
+    d->tokens = tokens;
+    d->head_dim = head_dim;
+    d->causal = causal;
+    d->in_dtype = SAB_F16;
+    d->out_dtype = SAB_F32;
+    d->block_q = kBlockQ;
+    d->block_kv = kBlockKV;
+    d->smooth_k = 1;
+    d->pv_accum = SAB_PV_FP32;
+    d->check_v = 0;
+}
+
+int sab_check_desc(const sab_desc* d) {
+    if (!d) return set_error(SAB_ERR_ARGUMENT, "sab_desc is NULL");
+    if (d->block_q < 1 || d->block_kv < 1)
+        return set_error(SAB_ERR_SHAPE, "sage_attention: block sizes must be >= 1");
+    if (d->batch < 1 || d->heads < 1 || d->tokens < 1 || d->head_dim < 1)
+        return set_error(SAB_ERR_SHAPE, "tensor dimensions must be positive");
+    if (d->head_dim != 64 && d->head_dim != 128)
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: head_dim must be 64 or 128 on the B200 path");
+    if (d->block_q != kBlockQ || d->block_kv != kBlockKV)
+        return set_error(SAB_ERR_UNSUPPORTED,
+                         "sage_attention: SAGEAttn-B uses block_q=128, block_kv=64 (kernel_config_for(B))");
+    if ((d->in_dtype != SAB_F16 && d->in_dtype != SAB_F32) || (d->out_dtype != SAB_F16 && d->out_dtype != SAB_F32))
+        return set_error(SAB_ERR_ARGUMENT, "sab_desc: dtype must be SAB_F16 or SAB_F32");
+    if (d->pv_accum != SAB_PV_FP32)
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: only the FP32-accumulator P~V arm is implemented");
+    if (units_of(d) > (int64_t(1) << 24))
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: batch*heads too large");
+    return SAB_OK;
+}
+
+int sab_workspace_layout(const sab_desc* d, sab_ws_layout* layout) {
+    int st = sab_check_desc(d);
+    if (st) return st;
+    if (!layout) return set_error(SAB_ERR_ARGUMENT, "layout is NULL");
+    return layout_of(d, layout);
+}
+
+int sab_workspace_size(const sab_desc* d, size_t* bytes) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    if (!bytes) return set_error(SAB_ERR_ARGUMENT, "bytes is NULL");
+    *bytes = size_t(L.total);
+    return SAB_OK;
+}
+
+int sab_prepass(const sab_desc* d, const void* q, const void* k, const void* v, void* ws, size_t ws_bytes,
+                void* stream) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    if (!q || !k) return set_error(SAB_ERR_ARGUMENT, "sab_prepass: q/k is NULL");
+    if ((d->in_dtype == SAB_F32 || d->check_v) && !v) return set_error(SAB_ERR_ARGUMENT, "sab_prepass: v is NULL");
+    if (!ws || ws_bytes < L.total) return set_error(SAB_ERR_WORKSPACE, "sab_prepass: workspace too small");
+    if (!aligned16(q) || !aligned16(k) || (v && !aligned16(v)) || !aligned16(ws))
+        return set_error(SAB_ERR_ARGUMENT, "sab_prepass: pointers must be 16-byte aligned");
+    return enqueue_prepass(d, L, q, k, v, ws, static_cast<cudaStream_t>(stream), true);
+}
+
+int sab_attention(const sab_desc* d, void* ws, size_t ws_bytes, const void* v, void* o, void* stream) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    if (!ws || ws_bytes < L.total) return set_error(SAB_ERR_WORKSPACE, "sab_attention: workspace too small");
+    if (!o || (d->in_dtype == SAB_F16 && !v)) return set_error(SAB_ERR_ARGUMENT, "sab_attention: v/o is NULL");
+    if (!aligned16(o) || (v && !aligned16(v))) return set_error(SAB_ERR_ARGUMENT, "sab_attention: misaligned v/o");
+    return enqueue_attention(d, L, ws, v, o, static_cast<cudaStream_t>(stream));
+}
+
+int sab_attention_fwd(const sab_desc* d, const void* q, const void* k, const void* v, void* o, void* ws,
+                      size_t ws_bytes, void* stream) {
+    int st = sab_prepass(d, q, k, v, ws, ws_bytes, stream);
+    if (st) return st;
+    return sab_attention(d, ws, ws_bytes, v, o, stream);
+}
+
+int sab_read_status(const sab_desc* d, const void* ws, void* stream, int* status) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    if (!ws || !status) return set_error(SAB_ERR_ARGUMENT, "sab_read_status: NULL argument");
+    int word = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(&word, at<int>(const_cast<void*>(ws), L.status), sizeof(int),
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_read_status");
+    *status = map_status_word(word);
+    return SAB_OK;
+}
+
+int sab_shard_plan(int units, int n_shards, int s, int* first, int* count) {
+    if (units < 0 || n_shards < 1 || s < 0 || s >= n_shards || !first || !count)
+        return set_error(SAB_ERR_ARGUMENT, "sab_shard_plan: bad argument");
+    const int base = units / n_shards, rem = units % n_shards;
+    *count = base + (s < rem ? 1 : 0);
+    *first = s * base + std::min(s, rem);
+    return SAB_OK;
+}
+
+int sab_diagnostics(const sab_desc* d, uint64_t* s_stage_macs, uint64_t* pv_stage_macs) {
+    if (!d || !s_stage_macs || !pv_stage_macs) return set_error(SAB_ERR_ARGUMENT, "sab_diagnostics: NULL argument");
+    if (d->block_q < 1 || d->block_kv < 1) return set_error(SAB_ERR_SHAPE, "sage_attention: block sizes must be >= 1");
+    if (d->batch < 1 || d->heads < 1 || d->tokens < 1 || d->head_dim < 1)
+        return set_error(SAB_ERR_SHAPE, "tensor dimensions must be positive");
+    // attention.hpp:396-404: every non-skipped (i, j) tile adds bq * bkv * d.
+    const int64_t n = d->tokens, bq = d->block_q, bkv = d->block_kv;
+    uint64_t per_unit = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += bq) {
+        const int64_t rows = std::min(bq, n - r0), r1 = r0 + rows - 1;
+        if (!d->causal) {
+            per_unit += uint64_t(rows) * uint64_t(n);
+            continue;
+        }
+        for (int64_t c0 = 0; c0 < n && c0 <= r1; c0 += bkv) per_unit += uint64_t(rows) * uint64_t(std::min(bkv, n - c0));
+    }
+    const uint64_t macs = per_unit * uint64_t(d->head_dim) * uint64_t(units_of(d));
+    *s_stage_macs = macs;
+    *pv_stage_macs = macs;
+    return SAB_OK;
+}
+
+int sab_device_count(int* count) {
+    if (!count) return set_error(SAB_ERR_ARGUMENT, "count is NULL");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return SAB_OK;
+    }
+    int c = 0;
+    for (int i = 0; i < n; ++i) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, i) == cudaSuccess && prop.major == 10 && prop.minor == 0) ++c;
+    }
+    *count = c;
+    return SAB_OK;
+}
+
+int sab_qk_int32_tiles(const sab_desc* d, const void* ws, int unit, int q_tile, int32_t* s_out, void* stream) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    const int ntq = (d->tokens + kBlockQ - 1) / kBlockQ;
+    if (!ws || !s_out || unit < 0 || unit >= units_of(d) || q_tile < 0 || q_tile >= ntq)
+        return set_error(SAB_ERR_ARGUMENT, "sab_qk_int32_tiles: bad argument");
+    AttnParams a = attn_params(d, L, ws, nullptr, nullptr);
+    if (d->in_dtype == SAB_F16) a.v16 = at<uint16_t>(const_cast<void*>(ws), L.qcodes);  // any valid mapping; V unused
+    a.s_dump = s_out;
+    a.dump_unit = unit;
+    a.dump_qtile = q_tile;
+    cudaError_t e = launch_qk_dump(a, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "sab_qk_int32_tiles");
+    return SAB_OK;
+}
+
+// ----------------------------------------------------------------- K3 host path
+namespace {
+
+// Per-device execution context of the host-buffer path: three streams
+// (H2D / compute / D2H), per-chunk events and grow-only device buffers.
+// Contexts are pooled so repeated calls do not pay cudaMalloc/stream
+// creation; a context is owned by one call at a time, so concurrent callers
+// never share buffers (the reference entry is re-entrant, attention.hpp:9-12).
+struct DevCtx {
+    int device = -1;
+    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_cmp;
+    uint8_t* buf = nullptr;
+    size_t buf_bytes = 0;
+};
+
+std::mutex g_pool_mu;
+std::vector<DevCtx*> g_pool;
+
+cudaError_t ctx_reserve(DevCtx* c, size_t bytes, int n_events) {
+    cudaError_t e = cudaSuccess;
+    if (!c->s_in) {
+        if ((e = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking)) != cudaSuccess)
+            return e;
+    }
+    while (int(c->ev_in.size()) < n_events) {
+        cudaEvent_t a, b;
+        if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
+        c->ev_in.push_back(a);
+        c->ev_cmp.push_back(b);
+    }
+    if (c->buf_bytes < bytes) {
+        if (c->buf) cudaFree(c->buf);
+        c->buf = nullptr;
+        c->buf_bytes = 0;
+        if ((e = cudaMalloc(&c->buf, bytes)) != cudaSuccess) return e;
+        c->buf_bytes = bytes;
+    }
+    return e;
+}
+
+DevCtx* ctx_acquire(int device) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (size_t i = 0; i < g_pool.size(); ++i) {
+        if (g_pool[i]->device == device) {
+            DevCtx* c = g_pool[i];
+            g_pool.erase(g_pool.begin() + i);
+            return c;
+        }
+    }
+    DevCtx* c = new DevCtx;
+    c->device = device;
+    return c;
+}
+
+void ctx_release(DevCtx* c) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(c);
+}
+
+struct ShardJob {
+    const sab_desc* desc;
+    const uint8_t *q, *k, *v;
+    uint8_t* o;
+    int device;
+    int first, count;
+    int status;
+    std::string error;
+};
+
+int run_shard_on(ShardJob* job, DevCtx* ctx) {
+    const sab_desc* D = job->desc;
+    const size_t in_e = elem_size(D->in_dtype), out_e = elem_size(D->out_dtype);
+    const size_t unit_elems = size_t(D->tokens) * D->head_dim;
+    // Chunks of whole units (~96 MB of inputs each) so that H2D of chunk c+1,
+    // compute of chunk c and D2H of chunk c-1 overlap on the three streams.
+    const size_t unit_in_bytes = 3 * unit_elems * in_e;
+    const int chunk = int(std::max<size_t>(1, std::min<size_t>(job->count, (96u << 20) / unit_in_bytes)));
+    const int n_chunks = (job->count + chunk - 1) / chunk;
+
+    sab_desc cd = *D;
+    cd.batch = 1;
+    cd.heads = chunk;
+    sab_ws_layout L;
+    layout_of(&cd, &L);
+
+    const size_t in_bytes = align_up(size_t(job->count) * unit_elems * in_e, 256);
+    const size_t out_bytes = align_up(size_t(job->count) * unit_elems * out_e, 256);
+    cudaError_t e = ctx_reserve(ctx, 3 * in_bytes + out_bytes + L.total, n_chunks);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_attention_fwd_host: device buffers");
+    uint8_t* dq = ctx->buf;
+    uint8_t* dk = dq + in_bytes;
+    uint8_t* dv = dk + in_bytes;
+    uint8_t* dout = dv + in_bytes;
+    uint8_t* ws = dout + out_bytes;
+
+    if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t), ctx->s_cmp)) != cudaSuccess)
+        return cuda_fail(e, "sab_attention_fwd_host: memset");
+    int st = SAB_OK;
+    for (int c = 0; c < n_chunks && st == SAB_OK; ++c) {
+        const int u0 = c * chunk, cu = std::min(chunk, job->count - u0);
+        const size_t ioff = size_t(u0) * unit_elems * in_e, ibytes = size_t(cu) * unit_elems * in_e;
+        const size_t ooff = size_t(u0) * unit_elems * out_e, obytes = size_t(cu) * unit_elems * out_e;
+        if ((e = cudaMemcpyAsync(dq + ioff, job->q + ioff, ibytes, cudaMemcpyHostToDevice, ctx->s_in)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dk + ioff, job->k + ioff, ibytes, cudaMemcpyHostToDevice, ctx->s_in)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dv + ioff, job->v + ioff, ibytes, cudaMemcpyHostToDevice, ctx->s_in)) != cudaSuccess ||
+            (e = cudaEventRecord(ctx->ev_in[c], ctx->s_in)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(ctx->s_cmp, ctx->ev_in[c], 0)) != cudaSuccess) {
+            st = cuda_fail(e, "sab_attention_fwd_host: H2D");
+            break;
+        }
+        sab_desc xd = cd;
+        xd.heads = cu;
+        sab_ws_layout XL;
+        layout_of(&xd, &XL);
+        XL.status = L.status;  // one status word for the whole shard
+        if ((st = enqueue_prepass(&xd, XL, dq + ioff, dk + ioff, dv + ioff, ws, ctx->s_cmp, false)) != SAB_OK) break;
+        if ((st = enqueue_attention(&xd, XL, ws, dv + ioff, dout + ooff, ctx->s_cmp)) != SAB_OK) break;
+        if ((e = cudaEventRecord(ctx->ev_cmp[c], ctx->s_cmp)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(ctx->s_out, ctx->ev_cmp[c], 0)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(job->o + ooff, dout + ooff, obytes, cudaMemcpyDeviceToHost, ctx->s_out)) !=
+                cudaSuccess) {
+            st = cuda_fail(e, "sab_attention_fwd_host: D2H");
+            break;
+        }
+    }
+    int word = 0;
+    if (st == SAB_OK &&
+        (e = cudaMemcpyAsync(&word, ws + L.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->s_cmp)) != cudaSuccess)
+        st = cuda_fail(e, "sab_attention_fwd_host: status");
+    // Always drain all three streams before the context is reused.
+    cudaError_t e1 = cudaStreamSynchronize(ctx->s_in), e2 = cudaStreamSynchronize(ctx->s_cmp),
+                e3 = cudaStreamSynchronize(ctx->s_out);
+    if (st == SAB_OK) {
+        e = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3);
+        if (e != cudaSuccess) return cuda_fail(e, "sab_attention_fwd_host: sync");
+        st = map_status_word(word);
+    }
+    return st;
+}
+
+void run_shard(ShardJob* job) {
+    cudaError_t e = cudaSetDevice(job->device);
+    int st;
+    if (e != cudaSuccess) {
+        st = cuda_fail(e, "cudaSetDevice");
+    } else {
+        DevCtx* ctx = ctx_acquire(job->device);
+        st = run_shard_on(job, ctx);
+        ctx_release(ctx);
+    }
+    job->status = st;
+    if (st != SAB_OK) job->error = g_last_error;
+}
+
+}  // namespace
+
+int sab_attention_fwd_host(const sab_desc* d, const void* q, const void* k, const void* v, void* o,
+                           const int* devices, int n_devices) {
+    int st = sab_check_desc(d);
+    if (st) return st;
+    if (!q || !k || !v || !o) return set_error(SAB_ERR_ARGUMENT, "sab_attention_fwd_host: NULL buffer");
+    int avail = 0;
+    if (cudaGetDeviceCount(&avail) != cudaSuccess || avail < 1)
+        return set_error(SAB_ERR_NO_DEVICE, "sab_attention_fwd_host: no CUDA device");
+    if (n_devices < 1) n_devices = 1;
+    std::vector<int> devs(n_devices);
+    for (int i = 0; i < n_devices; ++i) {
+        devs[i] = devices ? devices[i] : i;
+        if (devs[i] < 0 || devs[i] >= avail)
+            return set_error(SAB_ERR_NO_DEVICE, "sab_attention_fwd_host: device ordinal out of range");
+    }
+    const int units = int(units_of(d));
+    const size_t in_unit = size_t(d->tokens) * d->head_dim * elem_size(d->in_dtype);
+    const size_t out_unit = size_t(d->tokens) * d->head_dim * elem_size(d->out_dtype);
+    std::vector<ShardJob> jobs(n_devices);
+    for (int s = 0; s < n_devices; ++s) {
+        ShardJob& j = jobs[s];
+        j.desc = d;
+        j.device = devs[s];
+        sab_shard_plan(units, n_devices, s, &j.first, &j.count);
+        j.q = static_cast<const uint8_t*>(q) + j.first * in_unit;
+        j.k = static_cast<const uint8_t*>(k) + j.first * in_unit;
+        j.v = static_cast<const uint8_t*>(v) + j.first * in_unit;
+        j.o = static_cast<uint8_t*>(o) + j.first * out_unit;
+        j.status = SAB_OK;
+    }
+    if (n_devices == 1) {
+        if (jobs[0].count > 0) run_shard(&jobs[0]);
+    } else {
+        std::vector<std::thread> pool;
+        for (auto& j : jobs)
+            if (j.count > 0) pool.emplace_back(run_shard, &j);
+        for (auto& t : pool) t.join();
+    }
+    // Same precedence as the reference: validation errors before overflow.
+    int worst = SAB_OK;
+    std::string msg;
+    for (auto& j : jobs) {
+        if (j.status == SAB_OK) continue;
+        if (worst == SAB_OK || j.status == SAB_ERR_NONFINITE || (worst == SAB_ERR_OVERFLOW)) {
+            worst = j.status;
+            msg = j.error;
+        }
+    }
+    if (worst != SAB_OK) return set_error(worst, msg);
+    return SAB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// sab_internal.h -- launch parameters shared by the C-ABI layer and kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sageattn_b200.h"
+
+namespace sab {
+
+constexpr int kBlockQ = 128;    // query tile = Q quantization group (attention.hpp:51, 344)
+constexpr int kBlockKV = 64;    // K quantization group (attention.hpp:51, 345)
+constexpr int kTileN = 128;     // keys per K2 KV tile (two K groups)
+
+// Device status word bits (mapped to sab_status by sab_read_status).
+constexpr int kStatusNonFinite = 1;
+constexpr int kStatusOverflow = 2;
+
+struct PrepassParams {
+    const void* q;
+    const void* k;
+    const void* v;
+    int8_t* qcodes;
+    int8_t* kcodes;
+    float* qscales;
+    float* kscales;
+    float* mean;
+    float* partials;
+    uint16_t* v16;
+    int* status;
+    int units, n, d;
+    int depth;          // tree depth of the 4..9-token node level
+    int nodes_per_cta;  // nodes summed per mean-partial CTA (power of two)
+    int n_partials;     // 2^depth / nodes_per_cta
+    int smooth;
+    int check_v;
+    int in_f32;
+    float inv_n;        // 1.0f / float(N)          (quant.hpp:228)
+    float fold;         // float(1/sqrt(double(d)))  (quant.hpp:249)
+};
+
+// Mean-tree geometry for N tokens (quant.hpp:203-213): the smallest depth at
+// which every node holds <= 9 tokens (floor(N/2^depth) < 9).
+int tree_depth(int n);
+int nodes_per_cta(int depth);
+
+cudaError_t launch_prepass(const PrepassParams& p, cudaStream_t s);
+
+struct AttnParams {
+    const int8_t* qcodes;
+    const int8_t* kcodes;
+    const float* qscales;
+    const float* kscales;
+    const void* v16;
+    void* o;
+    int* status;
+    int32_t* s_dump;  // debug: INT32 S tiles of one (unit, q-tile)
+    int units, n, d, causal, out_f32;
+    int dump_unit, dump_qtile;
+};
+
+cudaError_t launch_attention(const AttnParams& p, cudaStream_t s);
+cudaError_t launch_qk_dump(const AttnParams& p, cudaStream_t s);
+
+}  // namespace sab

@@ -1,0 +1,372 @@
+// sab_prepass.cu -- K1, the fused SageAttn-B pre-pass (HBM-bound).
+//
+// Replaces, bit-exactly, the reference pre-processing of attention.hpp:336-360:
+//   smooth_k            quant.hpp:220-242 (pairwise_column_sum, quant.hpp:203-213)
+//   fold_scale_into_q   quant.hpp:246-252
+//   quantize(per_block(128 | 64), Int8)   quant.hpp:95-173
+//   V -> binary16 grid  attention.hpp:371-375 (fp32 inputs only; F9: hardware
+//                       cvt.rn.f16.f32 == round_to_half for finite floats)
+//
+// Two launches per call:
+//   k1_mean_partials  grid (n_partials, units): each CTA sums an aligned
+//                     subtree of 'nodes_per_cta' leaf-level nodes of the
+//                     reference's pairwise tree for all head_dim channels.
+//   k1_quantize       grid (ceil(N/128), units): re-combines the partials
+//                     with the top of the same tree (-> mean_k, bit-exact),
+//                     then quantizes one 128-token Q group and the two
+//                     64-token K groups of that chunk.
+//
+// Tree equivalence: with depth = the smallest k such that
+// floor(N/2^k) < 9, every node at that depth holds 4..9 tokens and every node
+// above it splits in two, so the reference recursion is a perfect binary tree
+// over 2^depth leaf nodes.  A leaf of <= 8 tokens is a sequential sum from
+// 0.0f; a 9-token leaf is (4 sequential) + (5 sequential).
+//
+// No fast-math anywhere: explicit __fmul_rn / __fsub_rn / __fdiv_rn /
+// __float2int_rn reproduce the reference's binary32 operations one for one.
+#include <cuda_fp16.h>
+
+#include "sab_internal.h"
+#include "sab_ptx.cuh"
+
+namespace sab {
+
+int tree_depth(int n) {
+    int depth = 0;
+    while ((n >> depth) >= 9) ++depth;
+    return depth;
+}
+
+int nodes_per_cta(int depth) {
+    const int nodes = 1 << depth;
+    return nodes < 128 ? nodes : 128;
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* src, float (&x)[8]);
+
+template <>
+__device__ __forceinline__ void load8<__half>(const __half* src, float (&x)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(h[i]);
+        x[2 * i] = f.x;
+        x[2 * i + 1] = f.y;
+    }
+}
+
+template <>
+__device__ __forceinline__ void load8<float>(const float* src, float (&x)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+
+__device__ __forceinline__ bool all_finite8(const float (&x)[8]) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ok &= isfinite(x[i]);
+    return ok;
+}
+
+// Token range [a, b) of leaf node `node` of the pairwise tree over [0, n):
+// descend `depth` levels, splitting [a, b) at a + (b - a) / 2 (quant.hpp:210).
+__device__ __forceinline__ void leaf_range(int node, int depth, int n, int& a, int& b) {
+    a = 0;
+    b = n;
+    for (int lv = depth - 1; lv >= 0; --lv) {
+        const int mid = a + (b - a) / 2;
+        if ((node >> lv) & 1) a = mid; else b = mid;
+    }
+}
+
+// Sequential binary32 sum from 0.0f of rows [t0, t1) (quant.hpp:205-208).
+template <typename T, int D>
+__device__ __forceinline__ void seq_sum(const T* base, int t0, int t1, int col, float (&s)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i] = 0.0f;
+    for (int t = t0; t < t1; ++t) {
+        float x[8];
+        load8<T>(base + static_cast<size_t>(t) * D + col, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = __fadd_rn(s[i], x[i]);
+    }
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
+    constexpr int CV = D / 8;           // 8-channel vectors per row
+    constexpr int NG = kThreads / CV;   // node groups per CTA
+    __shared__ float red[NG][D];
+
+    const int unit = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int cv = threadIdx.x % CV;
+    const int grp = threadIdx.x / CV;
+    const int active = p.nodes_per_cta / G;  // groups holding G nodes each
+    const T* base = static_cast<const T*>(p.k) + static_cast<size_t>(unit) * p.n * D;
+
+    if (grp < active) {
+        float ns[G][8];
+        const int node0 = chunk * p.nodes_per_cta + grp * G;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            int a, b;
+            leaf_range(node0 + g, p.depth, p.n, a, b);
+            if (b - a <= 8) {
+                seq_sum<T, D>(base, a, b, cv * 8, ns[g]);
+            } else {  // 9-token leaf: (4) + (5)
+                float lo[8], hi[8];
+                const int mid = a + (b - a) / 2;
+                seq_sum<T, D>(base, a, mid, cv * 8, lo);
+                seq_sum<T, D>(base, mid, b, cv * 8, hi);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ns[g][i] = __fadd_rn(lo[i], hi[i]);
+            }
+        }
+        // Perfect binary tree over the G nodes of this group (left + right).
+#pragma unroll
+        for (int step = 1; step < G; step *= 2)
+#pragma unroll
+            for (int g = 0; g < G; g += 2 * step)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ns[g][i] = __fadd_rn(ns[g][i], ns[g + step][i]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) red[grp][cv * 8 + i] = ns[0][i];
+    }
+    __syncthreads();
+    // Perfect binary tree over the active groups.
+    for (int stride = 1; stride < active; stride *= 2) {
+        if (grp < active && (grp % (2 * stride)) == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                red[grp][cv * 8 + i] = __fadd_rn(red[grp][cv * 8 + i], red[grp + stride][cv * 8 + i]);
+        }
+        __syncthreads();
+    }
+    if (grp == 0) {
+        float* dst = p.partials + (static_cast<size_t>(unit) * p.n_partials + chunk) * D + cv * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = red[0][cv * 8 + i];
+    }
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// quant.hpp:141-152: delta = amax / 127, inv = 1 / delta; zero group -> (1, 0).
+__device__ __forceinline__ void int8_scale(float amax, float& delta, float& inv) {
+    if (amax == 0.0f) {
+        delta = 1.0f;
+        inv = 0.0f;
+    } else {
+        delta = __fdiv_rn(amax, 127.0f);
+        inv = __fdiv_rn(1.0f, delta);
+    }
+}
+
+// quant.hpp:95-101: clamp(nearbyint(x * inv), -127, 127).
+__device__ __forceinline__ uint32_t code8(float x, float inv) {
+    int c = __float2int_rn(__fmul_rn(x, inv));
+    c = c > 127 ? 127 : (c < -127 ? -127 : c);
+    return static_cast<uint32_t>(c) & 0xFFu;
+}
+
+__device__ __forceinline__ uint2 codes8(const float (&x)[8], float inv) {
+    uint2 r;
+    r.x = code8(x[0], inv) | (code8(x[1], inv) << 8) | (code8(x[2], inv) << 16) | (code8(x[3], inv) << 24);
+    r.y = code8(x[4], inv) | (code8(x[5], inv) << 8) | (code8(x[6], inv) << 16) | (code8(x[7], inv) << 24);
+    return r;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads) k1_quantize(PrepassParams p) {
+    constexpr int CV = D / 8;
+    constexpr int VPT = kBlockQ * CV / kThreads;  // 8-element vectors per thread per 128-row chunk
+    constexpr int ROWS_PER_PASS = kThreads / CV;
+    __shared__ float s_mean[D];
+    __shared__ float s_red[kThreads / 32][3];
+    __shared__ float s_inv[3];
+
+    const int unit = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int r0 = chunk * kBlockQ;
+    const int rows = min(kBlockQ, p.n - r0);
+    const size_t ubase = static_cast<size_t>(unit) * p.n * D;
+
+    // 1. mean_k: top of the pairwise tree over the CTA partials (binary-counter
+    //    evaluation of a perfect tree, left + right), times 1.0f/N.
+    if (tid < D) {
+        float mean = 0.0f;
+        if (p.smooth) {
+            const float* part = p.partials + static_cast<size_t>(unit) * p.n_partials * D + tid;
+            float stk[24];
+            int top = 0;
+            for (int i = 0; i < p.n_partials; ++i) {
+                float x = part[static_cast<size_t>(i) * D];
+                for (int t = i; t & 1; t >>= 1) x = __fadd_rn(stk[--top], x);
+                stk[top++] = x;
+            }
+            mean = __fmul_rn(stk[0], p.inv_n);
+        }
+        s_mean[tid] = mean;
+        if (chunk == 0) p.mean[static_cast<size_t>(unit) * D + tid] = mean;
+    }
+
+    // 2. Load Q and K vectors of this 128-token chunk.
+    const bool f32 = p.in_f32 != 0;
+    float qv[VPT][8], kv[VPT][8];
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * kThreads;
+        const int row = v / CV, col = (v % CV) * 8;
+        if (row < rows) {
+            const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
+            load8<T>(static_cast<const T*>(p.q) + off, qv[i]);
+            load8<T>(static_cast<const T*>(p.k) + off, kv[i]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) qv[i][e] = kv[i][e] = 0.0f;
+        }
+    }
+    __syncthreads();  // s_mean ready
+
+    // 3. fold (Q) / smooth (K) and the group maxima.
+    float amax_q = 0.0f, amax_k0 = 0.0f, amax_k1 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * kThreads;
+        const int col = (v % CV) * 8;
+        finite &= all_finite8(qv[i]) && all_finite8(kv[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            qv[i][e] = __fmul_rn(qv[i][e], p.fold);
+            kv[i][e] = __fsub_rn(kv[i][e], s_mean[col + e]);
+            amax_q = fmaxf(amax_q, fabsf(qv[i][e]));
+            if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, fabsf(kv[i][e]));
+            else amax_k1 = fmaxf(amax_k1, fabsf(kv[i][e]));
+        }
+    }
+    // Rows past N were zero-filled: |0 - mean| must not enter the K maxima.
+    if (rows < kBlockQ) {
+        amax_k0 = amax_k1 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int row = (tid + i * kThreads) / CV;
+            if (row < rows)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, fabsf(kv[i][e]));
+                    else amax_k1 = fmaxf(amax_k1, fabsf(kv[i][e]));
+                }
+        }
+    }
+    amax_q = warp_max(amax_q);
+    amax_k0 = warp_max(amax_k0);
+    amax_k1 = warp_max(amax_k1);
+    if ((tid & 31) == 0) {
+        s_red[tid >> 5][0] = amax_q;
+        s_red[tid >> 5][1] = amax_k0;
+        s_red[tid >> 5][2] = amax_k1;
+    }
+    if (!finite) atomicOr(p.status, kStatusNonFinite);
+    __syncthreads();
+    if (tid < 3) {
+        float m = 0.0f;
+        for (int w = 0; w < kThreads / 32; ++w) m = fmaxf(m, s_red[w][tid]);
+        float delta, inv;
+        int8_scale(m, delta, inv);
+        s_inv[tid] = inv;
+        const int ngk = (p.n + kBlockKV - 1) / kBlockKV;
+        if (tid == 0) {
+            p.qscales[static_cast<size_t>(unit) * ((p.n + kBlockQ - 1) / kBlockQ) + chunk] = delta;
+        } else {
+            const int g = 2 * chunk + (tid - 1);
+            if (g < ngk) p.kscales[static_cast<size_t>(unit) * ngk + g] = delta;
+        }
+    }
+    __syncthreads();
+
+    // 4. codes
+    const float inv_q = s_inv[0], inv_k0 = s_inv[1], inv_k1 = s_inv[2];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int v = tid + i * kThreads;
+        const int row = v / CV, col = (v % CV) * 8;
+        if (row < rows) {
+            const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
+            *reinterpret_cast<uint2*>(p.qcodes + off) = codes8(qv[i], inv_q);
+            *reinterpret_cast<uint2*>(p.kcodes + off) = codes8(kv[i], i < VPT / 2 ? inv_k0 : inv_k1);
+        }
+    }
+
+    // 5. V: fp32 inputs -> fp16 grid (with the finiteness check); fp16 inputs
+    //    are only scanned when asked (validate_input, attention.hpp:101).
+    if (f32 || p.check_v) {
+        bool vfin = true;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int v = tid + i * kThreads;
+            const int row = v / CV, col = (v % CV) * 8;
+            if (row < rows) {
+                const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
+                float x[8];
+                load8<T>(static_cast<const T*>(p.v) + off, x);
+                vfin &= all_finite8(x);
+                if (f32) {
+                    uint4 h;
+                    h.x = pack_half2(x[0], x[1]);
+                    h.y = pack_half2(x[2], x[3]);
+                    h.z = pack_half2(x[4], x[5]);
+                    h.w = pack_half2(x[6], x[7]);
+                    *reinterpret_cast<uint4*>(p.v16 + off) = h;
+                }
+            }
+        }
+        if (!vfin) atomicOr(p.status, kStatusNonFinite);
+    }
+    (void)ROWS_PER_PASS;
+}
+
+template <typename T, int D>
+cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
+    constexpr int NG = kThreads / (D / 8);
+    if (p.smooth) {
+        const dim3 grid(p.n_partials, p.units);
+        const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
+        switch (g) {
+            case 1: k1_mean_partials<T, D, 1><<<grid, kThreads, 0, s>>>(p); break;
+            case 2: k1_mean_partials<T, D, 2><<<grid, kThreads, 0, s>>>(p); break;
+            case 4: k1_mean_partials<T, D, 4><<<grid, kThreads, 0, s>>>(p); break;
+            case 8: k1_mean_partials<T, D, 8><<<grid, kThreads, 0, s>>>(p); break;
+            default: return cudaErrorInvalidValue;
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const dim3 grid((p.n + kBlockQ - 1) / kBlockQ, p.units);
+    k1_quantize<T, D><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_prepass(const PrepassParams& p, cudaStream_t s) {
+    if (p.d == 128) return p.in_f32 ? launch_typed<float, 128>(p, s) : launch_typed<__half, 128>(p, s);
+    if (p.d == 64) return p.in_f32 ? launch_typed<float, 64>(p, s) : launch_typed<__half, 64>(p, s);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace sab
