@@ -348,7 +348,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * units_total * n * d * 2,
                 "d2h_bytes_per_step": units_total * n * d * 2,
                 "how": "sab_attention_fwd_host on pinned host buffers, wall clock, max over ranks"},
-        "gpu_launches": args.steps * 3,  # k1_mean_partials + k1_quantize + k2_attention
+        "gpu_launches": args.steps * 4,  # k1_mean_partials + k1_mean_final + k1_quantize + k2_attention
         "roofline": {"bound": "tensor", "achieved": k2_ach, "peak": p_mix, "unit": "TFLOP/s",
                      "frac": k2_ach / p_mix, "traffic": traffic, "kernel": "k2_attention",
                      "ms_per_launch": k2_mean_ms,

@@ -136,9 +136,10 @@ int sab_shard_plan(int units, int n_shards, int s, int* first, int* count);
 
 /* Debug/parity: runs K2's tcgen05 kind::i8 QK^T for query tile `q_tile` of
  * unit `unit` and writes the exact INT32 S tiles (what detail::int8_tile_nt
- * computes, attention.hpp:265-279) for every KV tile K2 visits, as
- * int32 [n_kv_tiles][128 rows][128 keys] into device buffer `s_out`
- * (n_kv_tiles = ceil(tokens/128), or q_tile+1 when causal).  Async. */
+ * computes, attention.hpp:265-279) for every 64-key KV tile K2 visits, as
+ * int32 [n_kv_tiles][128 rows][64 keys] into device buffer `s_out`
+ * (n_kv_tiles = ceil(tokens/64), or min(2*q_tile+2, ceil(tokens/64)) when
+ * causal).  Async. */
 int sab_qk_int32_tiles(const sab_desc* d, const void* ws, int unit, int q_tile, int32_t* s_out, void* stream);
 
 /* SageDiagnostics MAC counters (attention.hpp:58-69, 404, 445) for the

@@ -2,23 +2,33 @@
 //
 // Replaces the q-block / kv-block engine of attention.hpp:383-541:
 //   detail::int8_tile_nt (265-279)          -> tcgen05.mma kind::i8, INT32 accumulators in TMEM
-//   s = (float(acc) * dQ) * dK (409-414)    -> one FMUL per element with dQ*dK*log2(e)
-//   causal tile classes (79-94, 399-427)    -> fully masked KV tiles never issued; element
-//                                              mask only on the diagonal / ragged tail tile
-//   online softmax (429-443)                -> registers, one thread per query row, exp2 on MUFU
+//   s = (float(acc) * dQ) * dK (409-414)    -> one FFMA per element with dQ*dK*log2(e) (exp2 domain)
+//   causal tile classes (79-94, 399-427)    -> fully masked KV tiles are never issued; the element
+//                                              mask runs only on the diagonal / ragged tail tile
+//   online softmax (429-443)                -> registers, one thread per query row
 //   P~ V with binary16 operands (447-475)   -> P packed to fp16 into TMEM (aliasing S),
 //                                              tcgen05.mma kind::f16 with A from TMEM, V from SMEM,
 //                                              FP32 accumulator in TMEM (the pv_fp32_accumulator arm)
 //   O = diag(l)^-1 O + overflow check (524-540) -> epilogue from TMEM, status word on non-finite O
 //
-// One CTA = one (unit, 128-query tile).  Warp roles (192 threads):
-//   warps 0-3  softmax + epilogue (thread i owns query row i = TMEM lane i)
-//   warp  4    TMA producer (Q^ once; K^ and V per 128-key tile, STAGES-deep ring)
-//   warp  5    MMA issuer (single thread): QK^T(j) into S[j%2], then P(j-1)V(j-1) into O
-// TMEM (512 columns): S0 [0,128), S1 [128,256) int32; P(j) fp16x2 over S[j%2] [0,64);
-//                      O [256, 256+D) fp32.
-// Rescaling of O is lazy (only when a row max grows by more than 2^8), which
-// is exact in real arithmetic because l and O share the stale max.
+// One CTA = one unit x 256 query rows = two 128-row query tiles A and B that
+// share every K^/V tile.  KV tiles are 64 keys = one K quantization group
+// (attention.hpp:345), so each S tile has a single dequant factor.
+// Warp roles (608 threads):
+//   warps 0-7  softmax + epilogue of tile A, warps 8-15 of tile B: each warp owns 16
+//              query rows (16 TMEM lanes); threads t and t+16 split a row's 64 keys
+//              (tcgen05.ld 16x32bx2), so 4 softmax warps share each SM sub-partition
+//   warp  16   TMA producer (Q^ of both tiles once; K^ and V per 64-key tile, STAGES-deep ring)
+//   warp  17   MMA issuer of tile A, warp 18 MMA issuer of tile B (one thread each):
+//              QK_x(j+2) as soon as the softmax has read S_x(j), PV_x(j) once P_x(j) is written
+// TMEM (512 columns): S_x[b] = [128x + 64b, +64) int32, double-buffered per tile x;
+//                      O_A [256, 256+D), O_B [256+D, 256+2D) fp32 accumulators.
+// SMEM: P_x[b] fp16 128x64 (K-major, 128B swizzle), the A operand of the PV MMA.
+// Keeping P out of TMEM frees S_x(j) the moment the softmax has loaded it, so
+// the QK MMAs run two tiles ahead and both softmax warpgroups compute
+// concurrently without waiting on the tensor pipe.
+// Rescaling of O is lazy (only when a row max grows by more than 2^8), which is
+// exact in real arithmetic because l and O share the stale max.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -29,34 +39,180 @@ namespace sab {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kBN = kTileN;
-constexpr int kThreads = 192;
+constexpr int kBN = 64;    // keys per KV tile = one K scale group
+constexpr int kThreads = 608;  // 16 softmax warps + TMA + 2 MMA issuers
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
+constexpr int kMaskedAcc = -2147483647;    // sentinel below any reachable INT32 S value
+constexpr int kPolyPer16 = 4;              // exponentials (of 16) evaluated by exp2_poly2 on the FMA pipe
+constexpr float kMagicF = 12582912.0f;     // 2^23 + 2^22
+
+// ------------------------------------------------------------ packed fp32 math
+struct f2 {
+    float x, y;
+};
+
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("{\n\t.reg .b64 a, b, c, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+        "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+    f2 d;
+    asm("{\n\t.reg .b64 a, b, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
+// 2^x on the FMA pipe for a pair: x = j + f with j = rint(x), f in [-0.5, 0.5];
+// 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, below the
+// binary16 rounding P~ gets next); j is added to the exponent field.
+__device__ __forceinline__ f2 exp2_poly2(f2 x) {
+    x.x = fmaxf(x.x, -126.0f);
+    x.y = fmaxf(x.y, -126.0f);
+    const f2 t = fadd2(x, f2{kMagicF, kMagicF});                   // rint(x) in the low mantissa bits
+    const f2 f = ffma2(fadd2(t, f2{-kMagicF, -kMagicF}), f2{-1.0f, -1.0f}, x);  // x - rint(x), exact
+    f2 p = ffma2(f2{0.05517154186964035f, 0.05517154186964035f}, f, f2{0.24261118471622467f, 0.24261118471622467f});
+    p = ffma2(p, f, f2{0.6932610273361206f, 0.6932610273361206f});
+    p = ffma2(p, f, f2{0.9999280571937561f, 0.9999280571937561f});
+    return f2{__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+              __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23))};
+}
 
 template <int D>
 struct Cfg {
-    static constexpr int kStages = D == 128 ? 3 : 4;
+    static constexpr int kStages = D == 128 ? 4 : 6;
     static constexpr int kQBytes = kBM * D;
     static constexpr int kKBytes = kBN * D;
     static constexpr int kVBytes = kBN * D * 2;
     static constexpr int kVChunk = kBN * 64 * 2;  // one 64-column SW128 panel of V
+    static constexpr int kPBytes = kBM * kBN * 2; // one P tile, 128 rows x 128 B
     static constexpr uint32_t kSwizzleQK = D == 128 ? kSwizzle128B : kSwizzle64B;
     static constexpr uint32_t kSboQK = 8 * D;     // 8 rows of D int8
     static constexpr int kOffQ = 0;
-    static constexpr int kOffK = kOffQ + kQBytes;
+    static constexpr int kOffP = kOffQ + 2 * kQBytes;
+    static constexpr int kOffK = kOffP + 4 * kPBytes;
     static constexpr int kOffV = kOffK + kStages * kKBytes;
     static constexpr int kOffBar = kOffV + kStages * kVBytes;
-    static constexpr int kSmemBytes = kOffBar + 256 + 1024;  // barriers + alignment slack
+    static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // barriers + alignment slack
 };
 
-struct Bars {
+struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
     uint64_t q_full;
-    uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
-    uint64_t s_full[2], p_full[2];
-    uint64_t pv_done, o_final;
+    uint64_t k_full[6], k_empty[6], v_full[6], v_empty[6];
+    uint64_t s_full[2][2], s_free[2][2], p_full[2][2], pv_done[2][2], o_final[2];
     uint32_t tmem_base;
 };
+
+// Opaque copy: stops the compiler from keeping the 128 per-key mask predicates
+// of pass 1 alive (in registers) until pass 2.
+__device__ __forceinline__ int opaque(int v) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
+
+// Max of N INT32 accumulators: 4 independent chains.  With MASK, columns
+// >= lim are excluded.
+template <bool MASK, int N>
+__device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
+    int mi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mi[e] = kMaskedAcc;
+#pragma unroll
+    for (int c = 0; c < N; c += 8)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            int a = static_cast<int>(r[c + e]), b = static_cast<int>(r[c + 4 + e]);
+            if (MASK) {
+                a = (c + e >= lim) ? kMaskedAcc : a;
+                b = (c + 4 + e >= lim) ? kMaskedAcc : b;
+            }
+            mi[e] = max(mi[e], max(a, b));
+        }
+    return max(max(mi[0], mi[1]), max(mi[2], mi[3]));
+}
+
+// Softmax of one 64-key S tile row, shared by two threads of a warp: thread t
+// (< 16) holds keys [0, 32) and thread t + 16 keys [32, 64) of TMEM lane t
+// (tcgen05.ld 16x32bx2).  S holds INT32 accumulators of one K scale group with
+// dequant factor cg = dQ*dK*log2 e.  Once the row is in registers `s_free` is
+// arrived (the MMA warp may refill S).  P is written as fp16 into this thread's
+// half of its 128-byte row `prow` of a 128B-swizzled K-major tile (16-byte chunk
+// c of row r lives at chunk c ^ (r & 7)).  Updates the running max m (log2
+// units) and this thread's partial row sum l; returns the O rescale factor (1
+// when the warp skips the lazy rescale).  `dump` receives the raw half row.
+template <bool MASK, bool CAUSAL>
+__device__ __forceinline__ float softmax_half(uint32_t ts, uint32_t s_free, uint32_t prow, int swz, int half, float cg,
+                                              int kb, int qi, int n, float& m, float& l, bool& rescale,
+                                              int32_t* dump) {
+    // Keys kb + 32*half + c are valid for c < lim: key < N and, when causal, key <= query.
+    const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
+    uint32_t r[32];
+    tmem_ld16x2_32(ts, r);
+    tmem_wait_ld();
+    tc_fence_before();
+    mbar_arrive(s_free);
+    if (dump) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) *reinterpret_cast<int4*>(dump + c) = make_int4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+    }
+    // Row max on the INT32 accumulators: acc -> acc*cg is monotone for cg > 0, so
+    // this is the reference's binary32 row max (attention.hpp:431-432) up to the
+    // final scaling.  The two halves of a row meet by a shuffle.
+    int imax = group_max<MASK>(r, lim);
+    imax = max(imax, __shfl_xor_sync(0xffffffffu, imax, 16));
+    const float mx = (MASK && imax == kMaskedAcc) ? -INFINITY : static_cast<float>(imax) * cg;
+    const float m_new = fmaxf(m, mx);
+    rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
+    float alpha = 1.0f;
+    if (rescale) {
+        alpha = ex2(m - m_new);
+        m = m_new;
+    }
+    const float mref = (m == -INFINITY) ? 0.0f : m;
+    // p = 2^(float(acc) * cg - m) with float(acc) = bits(acc + 2^23 + 2^22) - (2^23 + 2^22),
+    // exact for |acc| < 2^22 (|acc| <= 127^2 * 128 here): one IADD + half an FFMA2 per element.
+    const f2 cg2{cg, cg};
+    const float bgs = -fmaf(kMagicF, cg, mref);
+    const f2 bg{bgs, bgs};
+    const int lim2 = MASK ? opaque(lim) : lim;
+    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // 16-byte chunk 4*half + q = keys [8q, 8q+8) of this half
+        uint32_t pk[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = 8 * q + 2 * i;
+            const f2 t = ffma2(f2{__uint_as_float(r[c] + kMagicI), __uint_as_float(r[c + 1] + kMagicI)}, cg2, bg);
+            f2 pp;
+            if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
+                pp = exp2_poly2(t);
+            } else {
+                pp = f2{ex2(t.x), ex2(t.y)};
+            }
+            if (MASK) {
+                pp.x = (c >= lim2) ? 0.0f : pp.x;
+                pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+            }
+            acc[i] = fadd2(acc[i], pp);
+            pk[i] = pack_half2(pp.x, pp.y);
+        }
+        st_shared_v4(prow + (((4 * half + q) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
+    }
+    const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+    l = fmaf(l, alpha, sum.x + sum.y);
+    return alpha;
+}
 
 template <int D, bool CAUSAL, bool OUT_F32, bool DUMP>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -64,10 +220,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
     using C = Cfg<D>;
     constexpr int S = C::kStages;
+    static_assert(sizeof(Bars) <= 512, "barrier block overflows its reservation");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
     const uint32_t sQ = smem_u32(smem + C::kOffQ);
+    const uint32_t sP = smem_u32(smem + C::kOffP);
     const uint32_t sK = smem_u32(smem + C::kOffK);
     const uint32_t sV = smem_u32(smem + C::kOffV);
 
@@ -76,49 +234,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n = p.n;
     const int ntq = (n + kBM - 1) / kBM;
     const int ntk = (n + kBN - 1) / kBN;
-    const int ngk = (n + kBlockKV - 1) / kBlockKV;
+    const int npair = (ntq + 1) / 2;
 
-    int unit, qt;
+    int unit, pair;
     if (DUMP) {
         unit = p.dump_unit;
-        qt = p.dump_qtile;
-    } else {  // longest query tiles first (causal work grows with qt)
+        pair = p.dump_qtile / 2;
+    } else {  // longest query-tile pairs first (causal work grows with the pair index)
         unit = blockIdx.x % p.units;
-        qt = ntq - 1 - static_cast<int>(blockIdx.x / p.units);
+        pair = npair - 1 - static_cast<int>(blockIdx.x / p.units);
     }
-    const int nkv = CAUSAL ? min(qt + 1, ntk) : ntk;
+    const int qt0 = 2 * pair;
+    const bool has_b = qt0 + 1 < ntq;
+    // Causal: query tile qt (rows < 128(qt+1)) needs KV tiles j with 64j <= 128qt + 127.
+    const int nkv_a = CAUSAL ? min(2 * qt0 + 2, ntk) : ntk;
+    const int nkv_b = has_b ? (CAUSAL ? min(2 * qt0 + 4, ntk) : ntk) : 0;
+    const int nkv = max(nkv_a, nkv_b);
 
     if (threadIdx.x == 0) {
         mbar_init(smem_u32(&bars->q_full), 1);
         for (int s = 0; s < S; ++s) {
             mbar_init(smem_u32(&bars->k_full[s]), 1);
-            mbar_init(smem_u32(&bars->k_empty[s]), 1);
+            mbar_init(smem_u32(&bars->k_empty[s]), 2);  // one arrival per MMA issuer
             mbar_init(smem_u32(&bars->v_full[s]), 1);
-            mbar_init(smem_u32(&bars->v_empty[s]), 1);
+            mbar_init(smem_u32(&bars->v_empty[s]), 2);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_u32(&bars->s_full[b]), 1);
-            mbar_init(smem_u32(&bars->p_full[b]), 128);
+        for (int x = 0; x < 2; ++x) {
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(smem_u32(&bars->s_full[x][b]), 1);
+                mbar_init(smem_u32(&bars->s_free[x][b]), 256);
+                mbar_init(smem_u32(&bars->p_full[x][b]), 256);
+                mbar_init(smem_u32(&bars->pv_done[x][b]), 1);
+            }
+            mbar_init(smem_u32(&bars->o_final[x]), 1);
         }
-        mbar_init(smem_u32(&bars->pv_done), 1);
-        mbar_init(smem_u32(&bars->o_final), 1);
         fence_barrier_init();
     }
-    if (warp == 4) tmem_alloc<512>(smem_u32(&bars->tmem_base));
+    if (warp == 16) tmem_alloc<512>(smem_u32(&bars->tmem_base));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
-    const uint32_t tO = tbase + 256;
 
-    if (warp == 4) {
+    if (warp == 16) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
-            mbar_arrive_expect_tx(smem_u32(&bars->q_full), C::kQBytes);
-            tma_load_3d(sQ, &tm_q, smem_u32(&bars->q_full), 0, qt * kBM, unit);
+            mbar_arrive_expect_tx(smem_u32(&bars->q_full), (has_b ? 2 : 1) * C::kQBytes);
+            tma_load_3d(sQ, &tm_q, smem_u32(&bars->q_full), 0, qt0 * kBM, unit);
+            if (has_b) tma_load_3d(sQ + C::kQBytes, &tm_q, smem_u32(&bars->q_full), 0, (qt0 + 1) * kBM, unit);
             for (int j = 0; j < nkv; ++j) {
                 const int s = j % S;
                 const uint32_t ph = (j / S) & 1;
@@ -134,174 +300,173 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 5) {
-        // ------------------------------------------------------------ MMA issuer
+    } else if (warp == 17 || warp == 18) {
+        // ------------------------------------------------------------ MMA issuer of tile x
+        const int x = warp - 17;
+        const int nkv_x = x == 0 ? nkv_a : nkv_b;
         if (lane == 0) {
             constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, kBN);
             constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
-            mbar_wait(smem_u32(&bars->q_full), 0);
+            // Descriptors are advanced by adding (byte offset >> 4) to the start-address field.
+            const uint64_t dq = make_smem_desc(sQ + x * C::kQBytes, 16, C::kSboQK, C::kSwizzleQK);
+            const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
+            const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
+            const uint64_t dp0 = make_smem_desc(sP + x * 2 * C::kPBytes, 16, 1024, kSwizzle128B);
+            const uint32_t t_s0 = tbase + x * 128;
+            const uint32_t t_o = tbase + 256 + x * D;
+            if (nkv_x > 0) mbar_wait(smem_u32(&bars->q_full), 0);
             tc_fence_after();
-            for (int j = 0; j <= nkv; ++j) {
-                if (j < nkv) {
-                    const int s = j % S;
-                    mbar_wait(smem_u32(&bars->k_full[s]), (j / S) & 1);
+            // QK_x(j) into S_x[j%2]: the buffer's previous tile j-2 must have been read.
+            auto issue_qk = [&](int j) {
+                const int s = j % S;
+                mbar_wait(smem_u32(&bars->k_full[s]), (j / S) & 1);
+                if (j < nkv_x) {
+                    if (j >= 2) mbar_wait(smem_u32(&bars->s_free[x][j & 1]), ((j - 2) >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t d_tmem = tbase + (j & 1) * 128;
+                    const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < D / 32; ++kk) {
-                        const uint64_t a = make_smem_desc(sQ + kk * 32, 16, C::kSboQK, C::kSwizzleQK);
-                        const uint64_t b = make_smem_desc(sK + s * C::kKBytes + kk * 32, 16, C::kSboQK, C::kSwizzleQK);
-                        umma_i8_ss(d_tmem, a, b, idesc_qk, kk > 0);
-                    }
+                    for (int kk = 0; kk < D / 32; ++kk)
+                        umma_i8_ss(t_s0 + (j & 1) * 64, dq + static_cast<uint64_t>(kk * 2),
+                                   dk + static_cast<uint64_t>(kk * 2), idesc_qk, kk > 0);
+                    umma_commit(smem_u32(&bars->s_full[x][j & 1]));
                     umma_commit(smem_u32(&bars->k_empty[s]));
-                    umma_commit(smem_u32(&bars->s_full[j & 1]));
+                } else {
+                    mbar_arrive(smem_u32(&bars->k_empty[s]));  // tile not used by this query tile
                 }
-                if (j >= 1) {
-                    const int jp = j - 1;
-                    const int sp = jp % S;
-                    mbar_wait(smem_u32(&bars->p_full[jp & 1]), (jp >> 1) & 1);
-                    mbar_wait(smem_u32(&bars->v_full[sp]), (jp / S) & 1);
+            };
+            if (nkv > 0) issue_qk(0);
+            if (nkv > 1) issue_qk(1);
+            for (int j = 0; j < nkv; ++j) {
+                if (j + 2 < nkv) issue_qk(j + 2);
+                const int s = j % S;
+                mbar_wait(smem_u32(&bars->v_full[s]), (j / S) & 1);
+                if (j < nkv_x) {  // O_x += P_x(j) V(j)
+                    mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
                     tc_fence_after();
-                    const uint32_t p_tmem = tbase + (jp & 1) * 128;
+                    const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
+                    const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * C::kPBytes) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < kBN / 16; ++kk) {
-                        const uint64_t b =
-                            make_smem_desc(sV + sp * C::kVBytes + kk * 2048, C::kVChunk, 1024, kSwizzle128B);
-                        umma_f16_ts(tO, p_tmem + kk * 8, b, idesc_pv, (jp > 0 || kk > 0) ? 1u : 0u);
-                    }
-                    umma_commit(smem_u32(&bars->v_empty[sp]));
-                    umma_commit(smem_u32(&bars->pv_done));
-                    if (jp == nkv - 1) umma_commit(smem_u32(&bars->o_final));
+                    for (int kk = 0; kk < kBN / 16; ++kk)
+                        umma_f16_ss(t_o, dp + static_cast<uint64_t>(kk * 2), dv + static_cast<uint64_t>(kk * (2048 >> 4)),
+                                    idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(smem_u32(&bars->pv_done[x][j & 1]));
+                    umma_commit(smem_u32(&bars->v_empty[s]));
+                    if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
+                } else {
+                    mbar_arrive(smem_u32(&bars->v_empty[s]));
                 }
             }
         }
         __syncwarp();
-    } else {
-        // ------------------------------------------------------------ softmax warps 0-3
-        const int row = warp * 32 + lane;
-        const uint32_t trow = tbase + (static_cast<uint32_t>(warp * 32) << 16);
+    } else if (warp < 16) {
+        // ------------------------------------------------------------ softmax warpgroups
+        // Tile x = warp / 8.  Warp w covers TMEM lanes [32(w%4) + 16((w%8)/4), +16); its
+        // threads t and t+16 share one query row (t % 16) and split the columns.
+        const int x = warp / 8;
+        const int qt = qt0 + x;
+        const int nkv_x = x == 0 ? nkv_a : nkv_b;
+        const int lane_base = (warp % 4) * 32 + ((warp % 8) / 4) * 16;
+        const int half = lane / 16;
+        const int row = lane_base + (lane % 16);
+        const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
+        const uint32_t t_o = tbase + lane_off + 256 + x * D;
+        const uint32_t prow0 = sP + x * 2 * C::kPBytes + row * 128;
         const int qi = qt * kBM + row;
-        const float qsl = p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
-        const float* ksc = p.kscales + static_cast<size_t>(unit) * ngk;
         float m = -INFINITY, l = 0.0f;
-
-        for (int j = 0; j < nkv; ++j) {
-            const int sb = j & 1;
-            mbar_wait(smem_u32(&bars->s_full[sb]), (j >> 1) & 1);
-            tc_fence_after();
-            uint32_t sr[kBN];
-#pragma unroll
-            for (int c = 0; c < kBN / 32; ++c) tmem_ld32(trow + sb * 128 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-            tmem_wait_ld();
-
-            if (DUMP) {
-                int32_t* dst = p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN;
-#pragma unroll
-                for (int c = 0; c < kBN; c += 4)
-                    *reinterpret_cast<int4*>(dst + c) = make_int4(sr[c], sr[c + 1], sr[c + 2], sr[c + 3]);
-            }
-
-            const int kb = j * kBN;
-            const int g0 = 2 * j;
-            const float c0 = qsl * ksc[g0];
-            const float c1 = (g0 + 1 < ngk) ? qsl * ksc[g0 + 1] : 0.0f;
-            float x[kBN];
-#pragma unroll
-            for (int c = 0; c < kBN; ++c) x[c] = static_cast<float>(static_cast<int32_t>(sr[c])) * (c < 64 ? c0 : c1);
-            const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
-            if (need_mask) {
-#pragma unroll
-                for (int c = 0; c < kBN; ++c) {
-                    const int key = kb + c;
-                    if (key >= n || (CAUSAL && key > qi)) x[c] = -INFINITY;
-                }
-            }
-            float mx = x[0];
-#pragma unroll
-            for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, x[c]);
-            const float m_new = fmaxf(m, mx);
-            const bool rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
-            float mu = m, alpha = 1.0f;
-            if (rescale) {
-                mu = m_new;
-                alpha = ex2(m - m_new);
-            }
-            const float mref = (mu == -INFINITY) ? 0.0f : mu;
-            float sum = 0.0f;
-            uint32_t pk[kBN / 2];
-#pragma unroll
-            for (int c = 0; c < kBN; c += 2) {
-                const float p0 = ex2(x[c] - mref);
-                const float p1 = ex2(x[c + 1] - mref);
-                sum += p0 + p1;
-                pk[c / 2] = pack_half2(p0, p1);
-            }
-            l = l * alpha + sum;
-            m = mu;
-
-            if (rescale && j > 0) {
-                // O must hold P(j-1)V(j-1) before it is rescaled; PV(j-2) is already
-                // complete (it precedes QK(j) in the tcgen05 pipe), so the pv_done phase
-                // counter is j-1 or j here and parity (j-1)&1 is unambiguous.
-                mbar_wait(smem_u32(&bars->pv_done), (j - 1) & 1);
+        if (nkv_x > 0) {
+            const float qsl = p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
+            const float* ksc = p.kscales + static_cast<size_t>(unit) * ntk;
+            // The K scale of the next KV tile is fetched one iteration ahead.
+            float ks_next = __ldg(ksc);
+            for (int j = 0; j < nkv_x; ++j) {
+                const float ks_cur = ks_next;
+                if (j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
+                const int b = j & 1;
+                mbar_wait(smem_u32(&bars->s_full[x][b]), (j >> 1) & 1);
                 tc_fence_after();
+                // P_x[b] is free once PV_x(j-2) has completed.
+                if (j >= 2) mbar_wait(smem_u32(&bars->pv_done[x][b]), ((j - 2) >> 1) & 1);
+                const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
+                const uint32_t s_free = smem_u32(&bars->s_free[x][b]);
+                const uint32_t prow = prow0 + b * C::kPBytes;
+                int32_t* dump = (DUMP && qt == p.dump_qtile)
+                                    ? p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN + 32 * half
+                                    : nullptr;
+                const int kb = j * kBN;
+                // Dequant factor of this 64-key group: dQ * dK * log2(e), so that p = 2^(s - m).
+                const float cg = qsl * ks_cur;
+                const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
+                bool rescale;
+                float alpha;
+                if (need_mask)
+                    alpha = softmax_half<true, CAUSAL>(t_s, s_free, prow, row & 7, half, cg, kb, qi, n, m, l, rescale,
+                                                       dump);
+                else
+                    alpha = softmax_half<false, CAUSAL>(t_s, s_free, prow, row & 7, half, cg, kb, qi, n, m, l, rescale,
+                                                        dump);
+                if (rescale && j > 0) {
+                    // O_x must hold P(j-1)V(j-1) before it is rescaled.  Thread halves split O's columns.
+                    mbar_wait(smem_u32(&bars->pv_done[x][(j - 1) & 1]), ((j - 1) >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < D / 2; c += 32) {
+                        uint32_t o[32];
+                        tmem_ld16x2_32o<D / 2>(t_o + c, o);
+                        tmem_wait_ld();
 #pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    uint32_t o[32];
-                    tmem_ld32(trow + 256 + c * 32, o);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tmem_st32(trow + 256 + c * 32, o);
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tmem_st16x2_32o<D / 2>(t_o + c, o);
+                    }
+                    tmem_wait_st();
                 }
+                fence_proxy_async_smem();  // P stores -> visible to the tensor core
+                tc_fence_before();
+                mbar_arrive(smem_u32(&bars->p_full[x][b]));
             }
-#pragma unroll
-            for (int c = 0; c < kBN / 64; ++c)
-                tmem_st32(trow + sb * 128 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(smem_u32(&bars->p_full[sb]));
-        }
 
-        // ------------------------------------------------------------ epilogue
-        mbar_wait(smem_u32(&bars->o_final), 0);
-        tc_fence_after();
-        if (!DUMP) {
-            const float inv_l = 1.0f / l;
-            bool finite = true;
+            // -------------------------------------------------------- epilogue
+            mbar_wait(smem_u32(&bars->o_final[x]), 0);
+            tc_fence_after();
+            l += __shfl_xor_sync(0xffffffffu, l, 16);  // the two column halves of the row
+            if (!DUMP) {
+                const float inv_l = 1.0f / l;
+                bool finite = true;
+#pragma unroll 1
+                for (int c = 0; c < D / 2; c += 32) {
+                    uint32_t o[32];
+                    tmem_ld16x2_32o<D / 2>(t_o + c, o);
+                    tmem_wait_ld();
+                    float v[32];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t o[32];
-                tmem_ld32(trow + 256 + c * 32, o);
-                tmem_wait_ld();
-                float v[32];
+                    for (int e = 0; e < 32; ++e) {
+                        finite &= isfinite(__uint_as_float(o[e]));
+                        v[e] = __uint_as_float(o[e]) * inv_l;
+                    }
+                    if (qi < n) {
+                        const size_t off = (static_cast<size_t>(unit) * n + qi) * D + half * (D / 2) + c;
+                        if (OUT_F32) {
+                            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    finite &= isfinite(__uint_as_float(o[e]));
-                    v[e] = __uint_as_float(o[e]) * inv_l;
-                }
-                if (qi < n) {
-                    const size_t off = (static_cast<size_t>(unit) * n + qi) * D + c * 32;
-                    if (OUT_F32) {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
+                            for (int e = 0; e < 8; ++e)
+                                dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+                        } else {
+                            uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                    } else {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
-                                                pack_half2(v[8 * e + 4], v[8 * e + 5]), pack_half2(v[8 * e + 6], v[8 * e + 7]));
+                            for (int e = 0; e < 4; ++e)
+                                dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
+                                                    pack_half2(v[8 * e + 4], v[8 * e + 5]),
+                                                    pack_half2(v[8 * e + 6], v[8 * e + 7]));
+                        }
                     }
                 }
+                if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
             }
-            if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
         }
     }
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 16) {
         tc_fence_after();
         tmem_dealloc<512>(tbase);
     }
@@ -324,14 +489,14 @@ EncodeFn get_encode() {
     return fn;
 }
 
-// (inner=d, tokens, units) tensor map with a (box_x, 128, 1) box.
+// (inner=d, tokens, units) tensor map with a (box_x, box_y, 1) box.
 bool make_map(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int elem, int d, int n, int units, int box_x,
-              CUtensorMapSwizzle sw) {
+              int box_y, CUtensorMapSwizzle sw) {
     EncodeFn enc = get_encode();
     if (!enc) return false;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(units)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * elem, static_cast<cuuint64_t>(d) * n * elem};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_x), 128, 1};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_x), static_cast<cuuint32_t>(box_y), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return enc(tm, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -342,15 +507,15 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     using C = Cfg<D>;
     CUtensorMap tq, tk, tv;
     const CUtensorMapSwizzle swqk = D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    if (!make_map(&tq, p.qcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, swqk) ||
-        !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, swqk) ||
-        !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!make_map(&tq, p.qcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBM, swqk) ||
+        !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBN, swqk) ||
+        !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, kBN, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int ntq = (p.n + kBM - 1) / kBM;
-    const unsigned grid = DUMP ? 1u : static_cast<unsigned>(ntq) * static_cast<unsigned>(p.units);
+    const unsigned grid = DUMP ? 1u : static_cast<unsigned>((ntq + 1) / 2) * static_cast<unsigned>(p.units);
     kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }

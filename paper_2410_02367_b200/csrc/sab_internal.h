@@ -11,7 +11,7 @@ namespace sab {
 
 constexpr int kBlockQ = 128;    // query tile = Q quantization group (attention.hpp:51, 344)
 constexpr int kBlockKV = 64;    // K quantization group (attention.hpp:51, 345)
-constexpr int kTileN = 128;     // keys per K2 KV tile (two K groups)
+constexpr int kTileN = 64;      // keys per K2 KV tile (one K group)
 
 // Device status word bits (mapped to sab_status by sab_read_status).
 constexpr int kStatusNonFinite = 1;

@@ -7,14 +7,15 @@
 //   V -> binary16 grid  attention.hpp:371-375 (fp32 inputs only; F9: hardware
 //                       cvt.rn.f16.f32 == round_to_half for finite floats)
 //
-// Two launches per call:
+// Three launches per call:
 //   k1_mean_partials  grid (n_partials, units): each CTA sums an aligned
 //                     subtree of 'nodes_per_cta' leaf-level nodes of the
 //                     reference's pairwise tree for all head_dim channels.
-//   k1_quantize       grid (ceil(N/128), units): re-combines the partials
-//                     with the top of the same tree (-> mean_k, bit-exact),
-//                     then quantizes one 128-token Q group and the two
-//                     64-token K groups of that chunk.
+//   k1_mean_final     grid (units): the top of the same tree over the CTA
+//                     partials -> mean_k (bit-exact).
+//   k1_quantize       grid (ceil(N/128), units): reads mean_k, then quantizes
+//                     one 128-token Q group and the two 64-token K groups of
+//                     that chunk.
 //
 // Tree equivalence: with depth = the smallest k such that
 // floor(N/2^k) < 9, every node at that depth holds 4..9 tokens and every node
@@ -39,7 +40,7 @@ int tree_depth(int n) {
 
 int nodes_per_cta(int depth) {
     const int nodes = 1 << depth;
-    return nodes < 128 ? nodes : 128;
+    return nodes < 32 ? nodes : 32;
 }
 
 namespace {
@@ -69,6 +70,39 @@ __device__ __forceinline__ void load8<float>(const float* src, float (&x)[8]) {
     x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
 
+// Raw 8-element vector as loaded (fp16: 16 B, fp32: 32 B), kept in registers
+// in its input format so K1 keeps Q and K of a 128-token chunk on chip.
+template <typename T>
+struct Raw8;
+template <>
+struct Raw8<__half> {
+    uint4 u;
+    __device__ __forceinline__ void load(const __half* src) { u = __ldg(reinterpret_cast<const uint4*>(src)); }
+    __device__ __forceinline__ void zero() { u = make_uint4(0, 0, 0, 0); }
+    __device__ __forceinline__ void get(float (&x)[8]) const {
+        const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(h[i]);
+            x[2 * i] = f.x;
+            x[2 * i + 1] = f.y;
+        }
+    }
+};
+template <>
+struct Raw8<float> {
+    float4 a, b;
+    __device__ __forceinline__ void load(const float* src) {
+        a = __ldg(reinterpret_cast<const float4*>(src));
+        b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+    }
+    __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+    __device__ __forceinline__ void get(float (&x)[8]) const {
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+};
+
 __device__ __forceinline__ bool all_finite8(const float (&x)[8]) {
     bool ok = true;
 #pragma unroll
@@ -87,16 +121,25 @@ __device__ __forceinline__ void leaf_range(int node, int depth, int n, int& a, i
     }
 }
 
-// Sequential binary32 sum from 0.0f of rows [t0, t1) (quant.hpp:205-208).
+// Sequential binary32 sum from 0.0f of rows [t0, t1), t1 - t0 <= 9
+// (quant.hpp:205-208).  All row loads are issued before the dependent adds.
 template <typename T, int D>
 __device__ __forceinline__ void seq_sum(const T* base, int t0, int t1, int col, float (&s)[8]) {
+    Raw8<T> v[9];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s[i] = 0.0f;
-    for (int t = t0; t < t1; ++t) {
-        float x[8];
-        load8<T>(base + static_cast<size_t>(t) * D + col, x);
+    for (int i = 0; i < 9; ++i) {
+        if (t0 + i < t1) v[i].load(base + static_cast<size_t>(t0 + i) * D + col);
+    }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] = __fadd_rn(s[i], x[i]);
+    for (int e = 0; e < 8; ++e) s[e] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        if (t0 + i < t1) {
+            float x[8];
+            v[i].get(x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], x[e]);
+        }
     }
 }
 
@@ -158,6 +201,32 @@ __global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
     }
 }
 
+// Top of the pairwise tree: combines the n_partials (power of two) CTA partial
+// sums of one unit as a perfect binary tree (binary-counter evaluation, left +
+// right), then mean = sum * (1.0f / N)  (quant.hpp:228, 235).
+template <int D>
+__global__ void __launch_bounds__(D) k1_mean_final(PrepassParams p) {
+    const int unit = blockIdx.x, c = threadIdx.x;
+    const float* part = p.partials + static_cast<size_t>(unit) * p.n_partials * D + c;
+    float stk[24];
+    int top = 0;
+    for (int i0 = 0; i0 < p.n_partials; i0 += 8) {  // n_partials is 1, 2, 4 or a multiple of 8
+        float xs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xs[u] = (i0 + u < p.n_partials) ? part[static_cast<size_t>(i0 + u) * D] : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u;
+            if (i < p.n_partials) {
+                float x = xs[u];
+                for (int t = i; t & 1; t >>= 1) x = __fadd_rn(stk[--top], x);
+                stk[top++] = x;
+            }
+        }
+    }
+    p.mean[static_cast<size_t>(unit) * D + c] = __fmul_rn(stk[0], p.inv_n);
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -189,11 +258,13 @@ __device__ __forceinline__ uint2 codes8(const float (&x)[8], float inv) {
     return r;
 }
 
+constexpr int kQThreads = 512;
+
 template <typename T, int D>
-__global__ void __launch_bounds__(kThreads) k1_quantize(PrepassParams p) {
+__global__ void __launch_bounds__(kQThreads, 1) k1_quantize(PrepassParams p) {
+    constexpr int kThreads = kQThreads;
     constexpr int CV = D / 8;
     constexpr int VPT = kBlockQ * CV / kThreads;  // 8-element vectors per thread per 128-row chunk
-    constexpr int ROWS_PER_PASS = kThreads / CV;
     __shared__ float s_mean[D];
     __shared__ float s_red[kThreads / 32][3];
     __shared__ float s_inv[3];
@@ -205,72 +276,44 @@ __global__ void __launch_bounds__(kThreads) k1_quantize(PrepassParams p) {
     const int rows = min(kBlockQ, p.n - r0);
     const size_t ubase = static_cast<size_t>(unit) * p.n * D;
 
-    // 1. mean_k: top of the pairwise tree over the CTA partials (binary-counter
-    //    evaluation of a perfect tree, left + right), times 1.0f/N.
-    if (tid < D) {
-        float mean = 0.0f;
-        if (p.smooth) {
-            const float* part = p.partials + static_cast<size_t>(unit) * p.n_partials * D + tid;
-            float stk[24];
-            int top = 0;
-            for (int i = 0; i < p.n_partials; ++i) {
-                float x = part[static_cast<size_t>(i) * D];
-                for (int t = i; t & 1; t >>= 1) x = __fadd_rn(stk[--top], x);
-                stk[top++] = x;
-            }
-            mean = __fmul_rn(stk[0], p.inv_n);
-        }
-        s_mean[tid] = mean;
-        if (chunk == 0) p.mean[static_cast<size_t>(unit) * D + tid] = mean;
-    }
-
-    // 2. Load Q and K vectors of this 128-token chunk.
-    const bool f32 = p.in_f32 != 0;
-    float qv[VPT][8], kv[VPT][8];
-    bool finite = true;
+    // 1. Issue every Q and K load of this 128-token chunk (kept raw in registers).
+    Raw8<T> qr[VPT], kr[VPT];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
         const int v = tid + i * kThreads;
         const int row = v / CV, col = (v % CV) * 8;
         if (row < rows) {
             const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
-            load8<T>(static_cast<const T*>(p.q) + off, qv[i]);
-            load8<T>(static_cast<const T*>(p.k) + off, kv[i]);
+            qr[i].load(static_cast<const T*>(p.q) + off);
+            kr[i].load(static_cast<const T*>(p.k) + off);
         } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) qv[i][e] = kv[i][e] = 0.0f;
+            qr[i].zero();
+            kr[i].zero();
         }
     }
-    __syncthreads();  // s_mean ready
+    // 2. mean_k (computed by k1_mean_final; zero when smoothing is off).
+    if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
+    __syncthreads();
 
-    // 3. fold (Q) / smooth (K) and the group maxima.
+    // 3. fold (Q) / smooth (K) and the group maxima.  Rows past N are excluded.
     float amax_q = 0.0f, amax_k0 = 0.0f, amax_k1 = 0.0f;
+    bool finite = true;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
         const int v = tid + i * kThreads;
-        const int col = (v % CV) * 8;
-        finite &= all_finite8(qv[i]) && all_finite8(kv[i]);
+        const int row = v / CV, col = (v % CV) * 8;
+        float q[8], k[8];
+        qr[i].get(q);
+        kr[i].get(k);
+        finite &= all_finite8(q) && all_finite8(k);
+        if (row < rows) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            qv[i][e] = __fmul_rn(qv[i][e], p.fold);
-            kv[i][e] = __fsub_rn(kv[i][e], s_mean[col + e]);
-            amax_q = fmaxf(amax_q, fabsf(qv[i][e]));
-            if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, fabsf(kv[i][e]));
-            else amax_k1 = fmaxf(amax_k1, fabsf(kv[i][e]));
-        }
-    }
-    // Rows past N were zero-filled: |0 - mean| must not enter the K maxima.
-    if (rows < kBlockQ) {
-        amax_k0 = amax_k1 = 0.0f;
-#pragma unroll
-        for (int i = 0; i < VPT; ++i) {
-            const int row = (tid + i * kThreads) / CV;
-            if (row < rows)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, fabsf(kv[i][e]));
-                    else amax_k1 = fmaxf(amax_k1, fabsf(kv[i][e]));
-                }
+            for (int e = 0; e < 8; ++e) {
+                amax_q = fmaxf(amax_q, fabsf(__fmul_rn(q[e], p.fold)));
+                const float ks = fabsf(__fsub_rn(k[e], s_mean[col + e]));
+                if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, ks);
+                else amax_k1 = fmaxf(amax_k1, ks);
+            }
         }
     }
     amax_q = warp_max(amax_q);
@@ -299,22 +342,30 @@ __global__ void __launch_bounds__(kThreads) k1_quantize(PrepassParams p) {
     }
     __syncthreads();
 
-    // 4. codes
+    // 4. codes (the binary32 fold / smooth is recomputed from the raw inputs).
     const float inv_q = s_inv[0], inv_k0 = s_inv[1], inv_k1 = s_inv[2];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
         const int v = tid + i * kThreads;
         const int row = v / CV, col = (v % CV) * 8;
         if (row < rows) {
+            float q[8], k[8];
+            qr[i].get(q);
+            kr[i].get(k);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                q[e] = __fmul_rn(q[e], p.fold);
+                k[e] = __fsub_rn(k[e], s_mean[col + e]);
+            }
             const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
-            *reinterpret_cast<uint2*>(p.qcodes + off) = codes8(qv[i], inv_q);
-            *reinterpret_cast<uint2*>(p.kcodes + off) = codes8(kv[i], i < VPT / 2 ? inv_k0 : inv_k1);
+            *reinterpret_cast<uint2*>(p.qcodes + off) = codes8(q, inv_q);
+            *reinterpret_cast<uint2*>(p.kcodes + off) = codes8(k, i < VPT / 2 ? inv_k0 : inv_k1);
         }
     }
 
     // 5. V: fp32 inputs -> fp16 grid (with the finiteness check); fp16 inputs
     //    are only scanned when asked (validate_input, attention.hpp:101).
-    if (f32 || p.check_v) {
+    if (p.in_f32 || p.check_v) {
         bool vfin = true;
 #pragma unroll
         for (int i = 0; i < VPT; ++i) {
@@ -325,7 +376,7 @@ __global__ void __launch_bounds__(kThreads) k1_quantize(PrepassParams p) {
                 float x[8];
                 load8<T>(static_cast<const T*>(p.v) + off, x);
                 vfin &= all_finite8(x);
-                if (f32) {
+                if (p.in_f32) {
                     uint4 h;
                     h.x = pack_half2(x[0], x[1]);
                     h.y = pack_half2(x[2], x[3]);
@@ -337,7 +388,6 @@ __global__ void __launch_bounds__(kThreads) k1_quantize(PrepassParams p) {
         }
         if (!vfin) atomicOr(p.status, kStatusNonFinite);
     }
-    (void)ROWS_PER_PASS;
 }
 
 template <typename T, int D>
@@ -346,18 +396,19 @@ cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
     if (p.smooth) {
         const dim3 grid(p.n_partials, p.units);
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
-        switch (g) {
+        switch (g) {  // nodes_per_cta() <= 32 -> at most 2 nodes per thread group
             case 1: k1_mean_partials<T, D, 1><<<grid, kThreads, 0, s>>>(p); break;
             case 2: k1_mean_partials<T, D, 2><<<grid, kThreads, 0, s>>>(p); break;
-            case 4: k1_mean_partials<T, D, 4><<<grid, kThreads, 0, s>>>(p); break;
-            case 8: k1_mean_partials<T, D, 8><<<grid, kThreads, 0, s>>>(p); break;
             default: return cudaErrorInvalidValue;
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+        k1_mean_final<D><<<p.units, D, 0, s>>>(p);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
     const dim3 grid((p.n + kBlockQ - 1) / kBlockQ, p.units);
-    k1_quantize<T, D><<<grid, kThreads, 0, s>>>(p);
+    k1_quantize<T, D><<<grid, kQThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -280,12 +280,12 @@ def attention_only_cuda(ws: Workspace, v, out, stream=None):
 
 
 def qk_int32_tiles_cuda(ws: Workspace, unit: int, q_tile: int, stream=None):
-    """INT32 S tiles K2 computes with tcgen05 kind::i8 for (unit, q_tile): int32 (n_kv_tiles, 128, 128)."""
+    """INT32 S tiles K2 computes with tcgen05 kind::i8 for (unit, q_tile): int32 (n_kv_tiles, 128, 64)."""
     torch = _torch()
     dsc = ws.desc
-    ntk = -(-dsc.tokens // 128)
-    nkv = min(q_tile + 1, ntk) if dsc.causal else ntk
-    out = torch.zeros((nkv, 128, 128), dtype=torch.int32, device=ws.buf.device)
+    ntk = -(-dsc.tokens // 64)
+    nkv = min(2 * q_tile + 2, ntk) if dsc.causal else ntk
+    out = torch.zeros((nkv, 128, 64), dtype=torch.int32, device=ws.buf.device)
     _lib.check(_lib.load().sab_qk_int32_tiles(C.byref(dsc), ws.ptr, unit, q_tile, out.data_ptr(),
                                               _stream_ptr(stream)))
     return out

@@ -43,7 +43,7 @@ def test_mean_tree_geometry(n, depth):
     L = _lib.workspace_layout(_lib.desc(1, 1, n, 64))
     assert L.tree_depth == depth
     assert (n >> depth) < 9 and (depth == 0 or (n >> (depth - 1)) >= 9)
-    assert L.n_partials * min(1 << depth, 128) == 1 << depth
+    assert L.n_partials * min(1 << depth, 32) == 1 << depth
 
 
 def test_workspace_layout_is_disjoint_and_aligned():

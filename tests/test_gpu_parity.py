@@ -83,7 +83,7 @@ def test_qk_int32_tiles_bit_exact(cuda, oracle, shape, causal):
             tiles = qk_int32_tiles_cuda(ws, unit, qt).cpu().numpy()
             r0, bq = qt * 128, min(128, n - qt * 128)
             for j in range(tiles.shape[0]):
-                c0, bkv = j * 128, min(128, n - j * 128)
+                c0, bkv = j * 64, min(64, n - j * 64)
                 ref = oracle.int8_tile(pre["qcodes"][unit], pre["kcodes"][unit], r0, bq, c0, bkv)
                 assert np.array_equal(tiles[j, :bq, :bkv], ref), (unit, qt, j)
 
