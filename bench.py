@@ -237,13 +237,20 @@ def main():
     from paper_2410_02367_b200 import _lib, sageattn, synth
 
     dist = None
+    n_dev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % max(1, n_dev))
+    torch.cuda.set_device(dev)
+    red_dev = dev
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
+        # One rank per GPU over NCCL; if ranks outnumber GPUs (functional runs on a
+        # 1-GPU box) the two host-side collectives (barrier, max of timings) use gloo.
+        if n_dev >= world:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+            red_dev = torch.device("cpu")
     first, count = _lib.shard_plan(units_total, world, rank)
 
     # Synthetic inputs of this rank's shard (global-index RNG: the shard equals the slice).
@@ -279,7 +286,7 @@ def main():
     torch.cuda.synchronize()
     _lib.check(sageattn.read_status(ws))
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev.index)
     t_step, t_k1, t_k2 = [], [], []
     with sampler:
         if dist:
@@ -302,15 +309,15 @@ def main():
         e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
         hq, hk, hv = (h.contiguous().pin_memory().numpy() for h in host)
         ho = torch.empty(hq.shape, dtype=torch.float16).pin_memory().numpy()
-        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[local_rank])  # warm the context pool
+        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index])  # warm the context pool
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[local_rank])
+            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index])
         e2e_s = time.perf_counter() - t0
 
-    local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s], dtype=torch.float64, device=dev)
+    local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s], dtype=torch.float64, device=red_dev)
     if dist:
         dist.all_reduce(local, op=dist.ReduceOp.MAX)
     tot_ms, k1_ms, k2_ms, e2e_max = local.tolist()
@@ -328,7 +335,7 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "k2_traffic.json")) as f:
-            tr = json.load(f).get(f"{args.workload}")
+            tr = json.load(f).get(f"{args.workload}")  # bytes per launch, whole job
             traffic = tr
     except (OSError, ValueError):
         pass

@@ -36,7 +36,31 @@
 #include "sab_ptx.cuh"
 
 namespace sab {
+
+#ifdef SAB_TRACE
+// Debug timeline (SAB_TRACE builds only): clock64 stamps of one CTA's pipeline
+// events, trace[(role * kTraceTiles + tile) * 8 + event].  Roles: 0/1 softmax
+// warp 0 of tile A/B, 2/3 MMA issuer of tile A/B, 4 TMA producer.
+__device__ long long* g_trace = nullptr;
+__device__ int g_trace_cta = 0;
+long long* h_trace_ptr = nullptr;
+int h_trace_cta = 0;
+#endif
+
 namespace {
+
+#ifdef SAB_TRACE
+constexpr int kTraceTiles = 512;
+#define SAB_STAMP(role, tile, ev)                                                                      \
+    do {                                                                                              \
+        if (g_trace && blockIdx.x == static_cast<unsigned>(g_trace_cta) && (tile) < kTraceTiles)      \
+            g_trace[((role) * kTraceTiles + (tile)) * 8 + (ev)] = clock64();                            \
+    } while (0)
+#else
+#define SAB_STAMP(role, tile, ev) \
+    do {                          \
+    } while (0)
+#endif
 
 constexpr int kBM = 128;
 constexpr int kBN = 64;    // keys per KV tile = one K scale group
@@ -45,7 +69,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
 constexpr int kMaskedAcc = -2147483647;    // sentinel below any reachable INT32 S value
-constexpr int kPolyPer16 = 4;              // exponentials (of 16) evaluated by exp2_poly2 on the FMA pipe
+#ifndef SAB_POLY_PER16
+#define SAB_POLY_PER16 0
+#endif
+constexpr int kPolyPer16 = SAB_POLY_PER16;  // exponentials (of 16) evaluated by exp2_poly2 on the FMA pipe
 constexpr float kMagicF = 12582912.0f;     // 2^23 + 2^22
 
 // ------------------------------------------------------------ packed fp32 math
@@ -148,20 +175,22 @@ __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
 // dequant factor cg = dQ*dK*log2 e.  Once the row is in registers `s_free` is
 // arrived (the MMA warp may refill S).  P is written as fp16 into this thread's
 // half of its 128-byte row `prow` of a 128B-swizzled K-major tile (16-byte chunk
-// c of row r lives at chunk c ^ (r & 7)).  Updates the running max m (log2
+// c of row r lives at chunk c ^ (r & 7)) once `p_free` (if non-zero) shows the
+// PV MMA two tiles back has consumed it.  Updates the running max m (log2
 // units) and this thread's partial row sum l; returns the O rescale factor (1
 // when the warp skips the lazy rescale).  `dump` receives the raw half row.
 template <bool MASK, bool CAUSAL>
-__device__ __forceinline__ float softmax_half(uint32_t ts, uint32_t s_free, uint32_t prow, int swz, int half, float cg,
-                                              int kb, int qi, int n, float& m, float& l, bool& rescale,
-                                              int32_t* dump) {
+__device__ __forceinline__ float softmax_half(uint32_t ts, uint32_t s_free, uint32_t p_free, uint32_t p_par,
+                                              uint32_t prow, int swz, int half, float cg, int kb, int qi, int n,
+                                              float& m, float& l, bool& rescale, int32_t* dump) {
     // Keys kb + 32*half + c are valid for c < lim: key < N and, when causal, key <= query.
     const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
     uint32_t r[32];
     tmem_ld16x2_32(ts, r);
     tmem_wait_ld();
     tc_fence_before();
-    mbar_arrive(s_free);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(s_free);  // one arrival per warp
     if (dump) {
 #pragma unroll
         for (int c = 0; c < 32; c += 4) *reinterpret_cast<int4*>(dump + c) = make_int4(r[c], r[c + 1], r[c + 2], r[c + 3]);
@@ -186,6 +215,7 @@ __device__ __forceinline__ float softmax_half(uint32_t ts, uint32_t s_free, uint
     const float bgs = -fmaf(kMagicF, cg, mref);
     const f2 bg{bgs, bgs};
     const int lim2 = MASK ? opaque(lim) : lim;
+    if (p_free) mbar_wait(p_free, p_par);  // the PV MMA two tiles back has read this P buffer
     f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // 16-byte chunk 4*half + q = keys [8q, 8q+8) of this half
@@ -262,8 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int x = 0; x < 2; ++x) {
             for (int b = 0; b < 2; ++b) {
                 mbar_init(smem_u32(&bars->s_full[x][b]), 1);
-                mbar_init(smem_u32(&bars->s_free[x][b]), 256);
-                mbar_init(smem_u32(&bars->p_full[x][b]), 256);
+                mbar_init(smem_u32(&bars->s_free[x][b]), 8);  // one arrival per softmax warp
+                mbar_init(smem_u32(&bars->p_full[x][b]), 8);
                 mbar_init(smem_u32(&bars->pv_done[x][b]), 1);
             }
             mbar_init(smem_u32(&bars->o_final[x]), 1);
@@ -288,10 +318,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < nkv; ++j) {
                 const int s = j % S;
                 const uint32_t ph = (j / S) & 1;
+                SAB_STAMP(4, j, 0);
                 mbar_wait(smem_u32(&bars->k_empty[s]), ph ^ 1);
+                SAB_STAMP(4, j, 1);
                 mbar_arrive_expect_tx(smem_u32(&bars->k_full[s]), C::kKBytes);
                 tma_load_3d(sK + s * C::kKBytes, &tm_k, smem_u32(&bars->k_full[s]), 0, j * kBN, unit);
                 mbar_wait(smem_u32(&bars->v_empty[s]), ph ^ 1);
+                SAB_STAMP(4, j, 2);
                 mbar_arrive_expect_tx(smem_u32(&bars->v_full[s]), C::kVBytes);
 #pragma unroll
                 for (int c = 0; c < D / 64; ++c)
@@ -319,7 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // QK_x(j) into S_x[j%2]: the buffer's previous tile j-2 must have been read.
             auto issue_qk = [&](int j) {
                 const int s = j % S;
+                SAB_STAMP(2 + x, j, 0);
                 mbar_wait(smem_u32(&bars->k_full[s]), (j / S) & 1);
+                SAB_STAMP(2 + x, j, 1);
                 if (j < nkv_x) {
                     if (j >= 2) mbar_wait(smem_u32(&bars->s_free[x][j & 1]), ((j - 2) >> 1) & 1);
                     tc_fence_after();
@@ -330,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    dk + static_cast<uint64_t>(kk * 2), idesc_qk, kk > 0);
                     umma_commit(smem_u32(&bars->s_full[x][j & 1]));
                     umma_commit(smem_u32(&bars->k_empty[s]));
+                    SAB_STAMP(2 + x, j, 2);
                 } else {
                     mbar_arrive(smem_u32(&bars->k_empty[s]));  // tile not used by this query tile
                 }
@@ -341,7 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = j % S;
                 mbar_wait(smem_u32(&bars->v_full[s]), (j / S) & 1);
                 if (j < nkv_x) {  // O_x += P_x(j) V(j)
+                    SAB_STAMP(2 + x, j, 3);
                     mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
+                    SAB_STAMP(2 + x, j, 4);
                     tc_fence_after();
                     const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
                     const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * C::kPBytes) >> 4);
@@ -352,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma_commit(smem_u32(&bars->pv_done[x][j & 1]));
                     umma_commit(smem_u32(&bars->v_empty[s]));
                     if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
+                    SAB_STAMP(2 + x, j, 5);
                 } else {
                     mbar_arrive(smem_u32(&bars->v_empty[s]));
                 }
@@ -382,10 +421,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float ks_cur = ks_next;
                 if (j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
                 const int b = j & 1;
+                const bool tr = (warp % 8) == 0 && lane == 0;
+                if (tr) SAB_STAMP(x, j, 0);
                 mbar_wait(smem_u32(&bars->s_full[x][b]), (j >> 1) & 1);
                 tc_fence_after();
-                // P_x[b] is free once PV_x(j-2) has completed.
-                if (j >= 2) mbar_wait(smem_u32(&bars->pv_done[x][b]), ((j - 2) >> 1) & 1);
+                if (tr) SAB_STAMP(x, j, 1);
+                if (tr) SAB_STAMP(x, j, 2);
+                // P_x[b] is free once PV_x(j-2) has completed (checked just before the P stores).
+                const uint32_t p_free = j >= 2 ? smem_u32(&bars->pv_done[x][b]) : 0u;
+                const uint32_t p_par = ((j - 2) >> 1) & 1;
                 const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
                 const uint32_t s_free = smem_u32(&bars->s_free[x][b]);
                 const uint32_t prow = prow0 + b * C::kPBytes;
@@ -399,11 +443,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool rescale;
                 float alpha;
                 if (need_mask)
-                    alpha = softmax_half<true, CAUSAL>(t_s, s_free, prow, row & 7, half, cg, kb, qi, n, m, l, rescale,
-                                                       dump);
+                    alpha = softmax_half<true, CAUSAL>(t_s, s_free, p_free, p_par, prow, row & 7, half, cg, kb, qi, n,
+                                                       m, l, rescale, dump);
                 else
-                    alpha = softmax_half<false, CAUSAL>(t_s, s_free, prow, row & 7, half, cg, kb, qi, n, m, l, rescale,
-                                                        dump);
+                    alpha = softmax_half<false, CAUSAL>(t_s, s_free, p_free, p_par, prow, row & 7, half, cg, kb, qi, n,
+                                                        m, l, rescale, dump);
                 if (rescale && j > 0) {
                     // O_x must hold P(j-1)V(j-1) before it is rescaled.  Thread halves split O's columns.
                     mbar_wait(smem_u32(&bars->pv_done[x][(j - 1) & 1]), ((j - 1) >> 1) & 1);
@@ -419,9 +463,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tmem_wait_st();
                 }
+                if (tr) SAB_STAMP(x, j, 3);
                 fence_proxy_async_smem();  // P stores -> visible to the tensor core
                 tc_fence_before();
-                mbar_arrive(smem_u32(&bars->p_full[x][b]));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));  // one arrival per warp
+                if (tr) SAB_STAMP(x, j, 4);
             }
 
             // -------------------------------------------------------- epilogue
@@ -516,6 +563,10 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const int ntq = (p.n + kBM - 1) / kBM;
     const unsigned grid = DUMP ? 1u : static_cast<unsigned>((ntq + 1) / 2) * static_cast<unsigned>(p.units);
+#ifdef SAB_TRACE
+    cudaMemcpyToSymbolAsync(g_trace, &h_trace_ptr, sizeof(h_trace_ptr), 0, cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(g_trace_cta, &h_trace_cta, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+#endif
     kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, p);
     return cudaGetLastError();
 }
@@ -545,3 +596,10 @@ cudaError_t launch_qk_dump(const AttnParams& p, cudaStream_t s) {
 }
 
 }  // namespace sab
+
+#ifdef SAB_TRACE
+extern "C" void sab_debug_set_trace(void* dev_buf, int cta) {
+    sab::h_trace_ptr = static_cast<long long*>(dev_buf);
+    sab::h_trace_cta = cta;
+}
+#endif

@@ -45,11 +45,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
                  : "memory");
 }
 
+// Non-blocking probe: true once the phase with parity `parity` has completed.
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 // Blocks until the phase with parity `parity` of the barrier has completed.
-// The suspend-time hint lets the hardware park the warp instead of re-issuing
-// the try_wait loop, so waiting warps do not steal issue slots from the
+// A non-blocking test_wait handles the common already-complete case cheaply;
+// otherwise try_wait with a suspend-time hint parks the warp instead of
+// re-issuing the loop, so waiting warps do not steal issue slots from the
 // softmax warps sharing their SM sub-partition.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (mbar_test(bar, parity)) return;
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "SAB_WAIT_%=:\n\t"

@@ -1,0 +1,69 @@
+// Drop-in check: an application written against the reference's
+// sageattn::sage_attention API, compiled against include/sageattn/attention.hpp
+// and linked with libsageattn_b200.so.
+//   dropin_test <B> <H> <N> <d> <causal> <q.bin> <k.bin> <v.bin> <out.bin>
+// Inputs/outputs are raw float32 (B,H,N,d).  Also exercises the reference's
+// error contract.  Prints "MACS <s> <pv>" and "ERRORS OK".
+#include <sageattn/attention.hpp>
+
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+
+static void read_into(const char* path, sageattn::Tensor4f& t) {
+    std::ifstream f(path, std::ios::binary);
+    f.read(reinterpret_cast<char*>(t.data.data()), std::streamsize(t.size() * sizeof(float)));
+    if (!f) throw std::runtime_error(std::string("cannot read ") + path);
+}
+
+template <typename E, typename F>
+static bool throws(F&& f, const char* needle) {
+    try {
+        f();
+    } catch (const E& e) {
+        return std::string(e.what()).find(needle) != std::string::npos;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main(int argc, char** argv) {
+    if (argc != 10) {
+        std::fprintf(stderr, "usage: %s B H N d causal q k v out\n", argv[0]);
+        return 2;
+    }
+    const int B = std::atoi(argv[1]), H = std::atoi(argv[2]), N = std::atoi(argv[3]), D = std::atoi(argv[4]);
+    sageattn::AttentionInput in{sageattn::Tensor4f(B, H, N, D), sageattn::Tensor4f(B, H, N, D),
+                                sageattn::Tensor4f(B, H, N, D), std::atoi(argv[5]) != 0};
+    read_into(argv[6], in.q);
+    read_into(argv[7], in.k);
+    read_into(argv[8], in.v);
+
+    sageattn::SageDiagnostics diag;
+    sageattn::SageOptions opts;
+    opts.diagnostics = &diag;
+    const sageattn::Tensor4f out = sageattn::sage_attention(in, sageattn::SageVariant::B, opts);
+    std::ofstream(argv[9], std::ios::binary)
+        .write(reinterpret_cast<const char*>(out.data.data()), std::streamsize(out.size() * sizeof(float)));
+    std::printf("MACS %llu %llu\n", (unsigned long long)diag.s_stage_macs, (unsigned long long)diag.pv_stage_macs);
+
+    bool ok = true;
+    sageattn::KernelConfig bad = sageattn::kernel_config_for(sageattn::SageVariant::B);
+    bad.block_kv = 0;
+    ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(in, bad); }, "block sizes must be >= 1");
+    sageattn::AttentionInput mism = in;
+    mism.v = sageattn::Tensor4f(B, H, N, D == 64 ? 128 : 64);
+    ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(mism, sageattn::SageVariant::B); },
+                                        "Q, K, V shapes differ");
+    sageattn::AttentionInput nan_in = in;
+    nan_in.k.data[nan_in.k.size() / 2] = std::nanf("");
+    ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(nan_in, sageattn::SageVariant::B); },
+                                        "non-finite input");
+    ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(in, sageattn::SageVariant::VB); },
+                                        "SAGEAttn-B");
+    ok &= sageattn::apply_causal_tiling(0, 2, 128, 64, 1000) == sageattn::TileKind::Skip;
+    std::printf(ok ? "ERRORS OK\n" : "ERRORS FAILED\n");
+    return ok ? 0 : 1;
+}
