@@ -20,13 +20,14 @@
 //              (tcgen05.ld 16x32bx2), so 4 softmax warps share each SM sub-partition
 //   warp  16   TMA producer (Q^ of both tiles once; K^ and V per 64-key tile, STAGES-deep ring)
 //   warp  17   MMA issuer of tile A, warp 18 MMA issuer of tile B (one thread each):
-//              QK_x(j+2) as soon as the softmax has read S_x(j), PV_x(j) once P_x(j) is written
-// TMEM (512 columns): S_x[b] = [128x + 64b, +64) int32, double-buffered per tile x;
+//              PV_x(j) once P_x(j) is in TMEM, then QK_x(j+2) into the same S buffer
+// TMEM (512 columns): S_x[b] = [128x + 64b, +64) int32, double-buffered per tile x,
+//                      with P_x(j) stored as fp16x2 over the first 32 columns of
+//                      S_x[j%2] (the A operand of the TMEM-sourced PV MMA);
 //                      O_A [256, 256+D), O_B [256+D, 256+2D) fp32 accumulators.
-// SMEM: P_x[b] fp16 128x64 (K-major, 128B swizzle), the A operand of the PV MMA.
-// Keeping P out of TMEM frees S_x(j) the moment the softmax has loaded it, so
-// the QK MMAs run two tiles ahead and both softmax warpgroups compute
-// concurrently without waiting on the tensor pipe.
+// The tensor pipe runs one thread's tcgen05 ops in order, so issuing QK_x(j+2)
+// after PV_x(j) keeps P_x(j) intact until it has been read, and QK_x(j+1) runs
+// while softmax x(j) computes.
 // Rescaling of O is lazy (only when a row max grows by more than 2^8), which is
 // exact in real arithmetic because l and O share the stale max.
 #include <cuda.h>
@@ -117,17 +118,15 @@ __device__ __forceinline__ f2 exp2_poly2(f2 x) {
 
 template <int D>
 struct Cfg {
-    static constexpr int kStages = D == 128 ? 4 : 6;
+    static constexpr int kStages = D == 128 ? 6 : 8;
     static constexpr int kQBytes = kBM * D;
     static constexpr int kKBytes = kBN * D;
     static constexpr int kVBytes = kBN * D * 2;
     static constexpr int kVChunk = kBN * 64 * 2;  // one 64-column SW128 panel of V
-    static constexpr int kPBytes = kBM * kBN * 2; // one P tile, 128 rows x 128 B
     static constexpr uint32_t kSwizzleQK = D == 128 ? kSwizzle128B : kSwizzle64B;
     static constexpr uint32_t kSboQK = 8 * D;     // 8 rows of D int8
     static constexpr int kOffQ = 0;
-    static constexpr int kOffP = kOffQ + 2 * kQBytes;
-    static constexpr int kOffK = kOffP + 4 * kPBytes;
+    static constexpr int kOffK = kOffQ + 2 * kQBytes;
     static constexpr int kOffV = kOffK + kStages * kKBytes;
     static constexpr int kOffBar = kOffV + kStages * kVBytes;
     static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // barriers + alignment slack
@@ -135,8 +134,8 @@ struct Cfg {
 
 struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
     uint64_t q_full;
-    uint64_t k_full[6], k_empty[6], v_full[6], v_empty[6];
-    uint64_t s_full[2][2], s_free[2][2], p_full[2][2], pv_done[2][2], o_final[2];
+    uint64_t k_full[8], k_empty[8], v_full[8], v_empty[8];
+    uint64_t s_full[2][2], p_full[2][2], pv_done[2], o_final[2];
     uint32_t tmem_base;
 };
 
@@ -172,25 +171,20 @@ __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
 // Softmax of one 64-key S tile row, shared by two threads of a warp: thread t
 // (< 16) holds keys [0, 32) and thread t + 16 keys [32, 64) of TMEM lane t
 // (tcgen05.ld 16x32bx2).  S holds INT32 accumulators of one K scale group with
-// dequant factor cg = dQ*dK*log2 e.  Once the row is in registers `s_free` is
-// arrived (the MMA warp may refill S).  P is written as fp16 into this thread's
-// half of its 128-byte row `prow` of a 128B-swizzled K-major tile (16-byte chunk
-// c of row r lives at chunk c ^ (r & 7)) once `p_free` (if non-zero) shows the
-// PV MMA two tiles back has consumed it.  Updates the running max m (log2
-// units) and this thread's partial row sum l; returns the O rescale factor (1
-// when the warp skips the lazy rescale).  `dump` receives the raw half row.
+// dequant factor cg = dQ*dK*log2 e.  P is written as fp16x2 over the first 32
+// columns of the same S region (tcgen05.st 16x32bx2: thread t's 16 packed pairs
+// go to columns [16*half, 16*half + 16)), the A operand of the PV MMA.  Updates
+// the running max m (log2 units) and this thread's partial row sum l; returns the
+// O rescale factor (1 when the warp skips the lazy rescale).  `dump` receives
+// the raw half row.
 template <bool MASK, bool CAUSAL>
-__device__ __forceinline__ float softmax_half(uint32_t ts, uint32_t s_free, uint32_t p_free, uint32_t p_par,
-                                              uint32_t prow, int swz, int half, float cg, int kb, int qi, int n,
-                                              float& m, float& l, bool& rescale, int32_t* dump) {
+__device__ __forceinline__ float softmax_half(uint32_t ts, int half, float cg, int kb, int qi, int n, float& m,
+                                              float& l, bool& rescale, int32_t* dump) {
     // Keys kb + 32*half + c are valid for c < lim: key < N and, when causal, key <= query.
     const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
     uint32_t r[32];
     tmem_ld16x2_32(ts, r);
     tmem_wait_ld();
-    tc_fence_before();
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(s_free);  // one arrival per warp
     if (dump) {
 #pragma unroll
         for (int c = 0; c < 32; c += 4) *reinterpret_cast<int4*>(dump + c) = make_int4(r[c], r[c + 1], r[c + 2], r[c + 3]);
@@ -215,30 +209,26 @@ __device__ __forceinline__ float softmax_half(uint32_t ts, uint32_t s_free, uint
     const float bgs = -fmaf(kMagicF, cg, mref);
     const f2 bg{bgs, bgs};
     const int lim2 = MASK ? opaque(lim) : lim;
-    if (p_free) mbar_wait(p_free, p_par);  // the PV MMA two tiles back has read this P buffer
     f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    uint32_t pk[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // 16-byte chunk 4*half + q = keys [8q, 8q+8) of this half
-        uint32_t pk[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int c = 8 * q + 2 * i;
-            const f2 t = ffma2(f2{__uint_as_float(r[c] + kMagicI), __uint_as_float(r[c + 1] + kMagicI)}, cg2, bg);
-            f2 pp;
-            if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
-                pp = exp2_poly2(t);
-            } else {
-                pp = f2{ex2(t.x), ex2(t.y)};
-            }
-            if (MASK) {
-                pp.x = (c >= lim2) ? 0.0f : pp.x;
-                pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
-            }
-            acc[i] = fadd2(acc[i], pp);
-            pk[i] = pack_half2(pp.x, pp.y);
+    for (int i = 0; i < 16; ++i) {
+        const int c = 2 * i;
+        const f2 t = ffma2(f2{__uint_as_float(r[c] + kMagicI), __uint_as_float(r[c + 1] + kMagicI)}, cg2, bg);
+        f2 pp;
+        if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
+            pp = exp2_poly2(t);
+        } else {
+            pp = f2{ex2(t.x), ex2(t.y)};
         }
-        st_shared_v4(prow + (((4 * half + q) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
+        if (MASK) {
+            pp.x = (c >= lim2) ? 0.0f : pp.x;
+            pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+        }
+        acc[i & 3] = fadd2(acc[i & 3], pp);
+        pk[i] = pack_half2(pp.x, pp.y);
     }
+    tmem_st16x2_16(ts, pk);
     const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
     l = fmaf(l, alpha, sum.x + sum.y);
     return alpha;
@@ -255,7 +245,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
     const uint32_t sQ = smem_u32(smem + C::kOffQ);
-    const uint32_t sP = smem_u32(smem + C::kOffP);
     const uint32_t sK = smem_u32(smem + C::kOffK);
     const uint32_t sV = smem_u32(smem + C::kOffV);
 
@@ -292,10 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int x = 0; x < 2; ++x) {
             for (int b = 0; b < 2; ++b) {
                 mbar_init(smem_u32(&bars->s_full[x][b]), 1);
-                mbar_init(smem_u32(&bars->s_free[x][b]), 8);  // one arrival per softmax warp
-                mbar_init(smem_u32(&bars->p_full[x][b]), 8);
-                mbar_init(smem_u32(&bars->pv_done[x][b]), 1);
+                mbar_init(smem_u32(&bars->p_full[x][b]), 8);  // one arrival per softmax warp
             }
+            mbar_init(smem_u32(&bars->pv_done[x]), 1);
             mbar_init(smem_u32(&bars->o_final[x]), 1);
         }
         fence_barrier_init();
@@ -344,19 +332,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dq = make_smem_desc(sQ + x * C::kQBytes, 16, C::kSboQK, C::kSwizzleQK);
             const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
             const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
-            const uint64_t dp0 = make_smem_desc(sP + x * 2 * C::kPBytes, 16, 1024, kSwizzle128B);
             const uint32_t t_s0 = tbase + x * 128;
             const uint32_t t_o = tbase + 256 + x * D;
             if (nkv_x > 0) mbar_wait(smem_u32(&bars->q_full), 0);
             tc_fence_after();
-            // QK_x(j) into S_x[j%2]: the buffer's previous tile j-2 must have been read.
+            // QK_x(j) into S_x[j%2].  Issued after PV_x(j-2), which read P_x(j-2) from that
+            // buffer (tcgen05 ops of one thread execute in issue order).
             auto issue_qk = [&](int j) {
                 const int s = j % S;
                 SAB_STAMP(2 + x, j, 0);
                 mbar_wait(smem_u32(&bars->k_full[s]), (j / S) & 1);
                 SAB_STAMP(2 + x, j, 1);
                 if (j < nkv_x) {
-                    if (j >= 2) mbar_wait(smem_u32(&bars->s_free[x][j & 1]), ((j - 2) >> 1) & 1);
                     tc_fence_after();
                     const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
 #pragma unroll
@@ -373,27 +360,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (nkv > 0) issue_qk(0);
             if (nkv > 1) issue_qk(1);
             for (int j = 0; j < nkv; ++j) {
-                if (j + 2 < nkv) issue_qk(j + 2);
                 const int s = j % S;
                 mbar_wait(smem_u32(&bars->v_full[s]), (j / S) & 1);
-                if (j < nkv_x) {  // O_x += P_x(j) V(j)
+                if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
                     SAB_STAMP(2 + x, j, 3);
                     mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
                     SAB_STAMP(2 + x, j, 4);
                     tc_fence_after();
                     const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
-                    const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * C::kPBytes) >> 4);
+                    const uint32_t t_p = t_s0 + (j & 1) * 64;
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk)
-                        umma_f16_ss(t_o, dp + static_cast<uint64_t>(kk * 2), dv + static_cast<uint64_t>(kk * (2048 >> 4)),
-                                    idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(smem_u32(&bars->pv_done[x][j & 1]));
+                        umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
+                                    (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(smem_u32(&bars->pv_done[x]));
                     umma_commit(smem_u32(&bars->v_empty[s]));
                     if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
                     SAB_STAMP(2 + x, j, 5);
                 } else {
                     mbar_arrive(smem_u32(&bars->v_empty[s]));
                 }
+                if (j + 2 < nkv) issue_qk(j + 2);
             }
         }
         __syncwarp();
@@ -409,7 +396,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = lane_base + (lane % 16);
         const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
         const uint32_t t_o = tbase + lane_off + 256 + x * D;
-        const uint32_t prow0 = sP + x * 2 * C::kPBytes + row * 128;
         const int qi = qt * kBM + row;
         float m = -INFINITY, l = 0.0f;
         if (nkv_x > 0) {
@@ -426,13 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(smem_u32(&bars->s_full[x][b]), (j >> 1) & 1);
                 tc_fence_after();
                 if (tr) SAB_STAMP(x, j, 1);
-                if (tr) SAB_STAMP(x, j, 2);
-                // P_x[b] is free once PV_x(j-2) has completed (checked just before the P stores).
-                const uint32_t p_free = j >= 2 ? smem_u32(&bars->pv_done[x][b]) : 0u;
-                const uint32_t p_par = ((j - 2) >> 1) & 1;
                 const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
-                const uint32_t s_free = smem_u32(&bars->s_free[x][b]);
-                const uint32_t prow = prow0 + b * C::kPBytes;
                 int32_t* dump = (DUMP && qt == p.dump_qtile)
                                     ? p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN + 32 * half
                                     : nullptr;
@@ -443,14 +423,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool rescale;
                 float alpha;
                 if (need_mask)
-                    alpha = softmax_half<true, CAUSAL>(t_s, s_free, p_free, p_par, prow, row & 7, half, cg, kb, qi, n,
-                                                       m, l, rescale, dump);
+                    alpha = softmax_half<true, CAUSAL>(t_s, half, cg, kb, qi, n, m, l, rescale, dump);
                 else
-                    alpha = softmax_half<false, CAUSAL>(t_s, s_free, p_free, p_par, prow, row & 7, half, cg, kb, qi, n,
-                                                        m, l, rescale, dump);
+                    alpha = softmax_half<false, CAUSAL>(t_s, half, cg, kb, qi, n, m, l, rescale, dump);
+                if (tr) SAB_STAMP(x, j, 2);
                 if (rescale && j > 0) {
-                    // O_x must hold P(j-1)V(j-1) before it is rescaled.  Thread halves split O's columns.
-                    mbar_wait(smem_u32(&bars->pv_done[x][(j - 1) & 1]), ((j - 1) >> 1) & 1);
+                    // O_x must hold P(j-1)V(j-1) before it is rescaled.  PV_x(j-2) is complete
+                    // (QK_x(j) was issued after it), so parity (j-1)&1 of pv_done is unambiguous.
+                    // Thread halves split O's columns.
+                    mbar_wait(smem_u32(&bars->pv_done[x]), (j - 1) & 1);
                     tc_fence_after();
 #pragma unroll 1
                     for (int c = 0; c < D / 2; c += 32) {
@@ -461,10 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
                         tmem_st16x2_32o<D / 2>(t_o + c, o);
                     }
-                    tmem_wait_st();
                 }
+                tmem_wait_st();  // P (and rescaled O) are in TMEM
                 if (tr) SAB_STAMP(x, j, 3);
-                fence_proxy_async_smem();  // P stores -> visible to the tensor core
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));  // one arrival per warp

@@ -236,6 +236,17 @@ __device__ __forceinline__ void tmem_st16x2_32o(uint32_t taddr, const uint32_t (
         : "memory");
 }
 
+// 16 lanes x (2 x 16 columns) store: thread t < 16 writes columns [0, 16) of
+// lane t, thread t >= 16 columns [16, 32) of lane t - 16.
+__device__ __forceinline__ void tmem_st16x2_16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], 16, "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 // Fills 32 consecutive columns of this warp's 32 lanes with the same value.
 __device__ __forceinline__ void tmem_fill32(uint32_t taddr, uint32_t v) {
     asm volatile(
