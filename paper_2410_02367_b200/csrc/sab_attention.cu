@@ -19,7 +19,7 @@
 //              query rows (16 TMEM lanes); threads t and t+16 split a row's 64 keys
 //              (tcgen05.ld 16x32bx2), so 4 softmax warps share each SM sub-partition
 //   warp  16   TMA producer (Q^ of both tiles once; K^ and V per 64-key tile, STAGES-deep ring)
-//   warp  17   MMA issuer of tile A, warp 18 MMA issuer of tile B (one thread each):
+//   warp  17   MMA issuer of tile A, warp 18 MMA issuer of tile B (whole warp, one elected lane issues):
 //              PV_x(j) once P_x(j) is in TMEM, then QK_x(j+2) into the same S buffer
 // TMEM (512 columns): S_x[b] = [128x + 64b, +64) int32, double-buffered per tile x,
 //                      with P_x(j) stored as fp16x2 over the first 32 columns of
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ MMA issuer of tile x
         const int x = warp - 17;
         const int nkv_x = x == 0 ? nkv_a : nkv_b;
-        if (lane == 0) {
+        {  // the whole warp runs the loop (uniform operands); one elected lane issues
             constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, kBN);
             constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
             // Descriptors are advanced by adding (byte offset >> 4) to the start-address field.
@@ -340,21 +340,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             // buffer (tcgen05 ops of one thread execute in issue order).
             auto issue_qk = [&](int j) {
                 const int s = j % S;
-                SAB_STAMP(2 + x, j, 0);
+                if (lane == 0) SAB_STAMP(2 + x, j, 0);
                 mbar_wait(smem_u32(&bars->k_full[s]), (j / S) & 1);
-                SAB_STAMP(2 + x, j, 1);
+                if (lane == 0) SAB_STAMP(2 + x, j, 1);
                 if (j < nkv_x) {
                     tc_fence_after();
                     const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
 #pragma unroll
                     for (int kk = 0; kk < D / 32; ++kk)
-                        umma_i8_ss(t_s0 + (j & 1) * 64, dq + static_cast<uint64_t>(kk * 2),
+                        umma_i8_ss_w(t_s0 + (j & 1) * 64, dq + static_cast<uint64_t>(kk * 2),
                                    dk + static_cast<uint64_t>(kk * 2), idesc_qk, kk > 0);
-                    umma_commit(smem_u32(&bars->s_full[x][j & 1]));
-                    umma_commit(smem_u32(&bars->k_empty[s]));
-                    SAB_STAMP(2 + x, j, 2);
+                    umma_commit_w(smem_u32(&bars->s_full[x][j & 1]));
+                    umma_commit_w(smem_u32(&bars->k_empty[s]));
+                    if (lane == 0) SAB_STAMP(2 + x, j, 2);
                 } else {
-                    mbar_arrive(smem_u32(&bars->k_empty[s]));  // tile not used by this query tile
+                    mbar_arrive_w(smem_u32(&bars->k_empty[s]));  // tile not used by this query tile
                 }
             };
             if (nkv > 0) issue_qk(0);
@@ -363,22 +363,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = j % S;
                 mbar_wait(smem_u32(&bars->v_full[s]), (j / S) & 1);
                 if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
-                    SAB_STAMP(2 + x, j, 3);
+                    if (lane == 0) SAB_STAMP(2 + x, j, 3);
                     mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
-                    SAB_STAMP(2 + x, j, 4);
+                    if (lane == 0) SAB_STAMP(2 + x, j, 4);
                     tc_fence_after();
                     const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
                     const uint32_t t_p = t_s0 + (j & 1) * 64;
 #pragma unroll
                     for (int kk = 0; kk < kBN / 16; ++kk)
-                        umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
+                        umma_f16_ts_w(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
                                     (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(smem_u32(&bars->pv_done[x]));
-                    umma_commit(smem_u32(&bars->v_empty[s]));
-                    if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
-                    SAB_STAMP(2 + x, j, 5);
+                    umma_commit_w(smem_u32(&bars->pv_done[x]));
+                    umma_commit_w(smem_u32(&bars->v_empty[s]));
+                    if (j == nkv_x - 1) umma_commit_w(smem_u32(&bars->o_final[x]));
+                    if (lane == 0) SAB_STAMP(2 + x, j, 5);
                 } else {
-                    mbar_arrive(smem_u32(&bars->v_empty[s]));
+                    mbar_arrive_w(smem_u32(&bars->v_empty[s]));
                 }
                 if (j + 2 < nkv) issue_qk(j + 2);
             }
