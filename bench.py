@@ -195,17 +195,24 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=None)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: N ranks run N x the workload's batch (fixed units per GPU); "
+                         "strong: the workload as given, head x batch sharded over the ranks")
     args = ap.parse_args()
     wl = workload(args.workload)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    units_total = wl["batch"] * wl["heads"]
+    batch = wl["batch"] * (world if args.scaling == "weak" else 1)
+    units_total = batch * wl["heads"]
     n, d, causal = wl["tokens"], wl["head_dim"], wl["causal"]
     total_ops = paper_ops(units_total, n, d, causal)
-    config = {"workload": wl["name"], "batch": wl["batch"], "heads": wl["heads"], "tokens": n, "head_dim": d,
-              "causal": causal, "parallelism": f"head-shard x{world}" if world > 1 else "single GPU",
+    config = {"workload": wl["name"], "batch": batch, "heads": wl["heads"], "tokens": n, "head_dim": d,
+              "causal": causal, "global_batch": batch,
+              "parallelism": (f"head x batch shard over {world} GPUs, no collective" if world > 1 else "single GPU"),
+              "scaling_mode": args.scaling + (" (batch grows with GPUs; units per GPU fixed)" if args.scaling == "weak"
+                                              else " (fixed workload sharded)"),
               "l2": "inputs (3 x fp16 Q/K/V) larger than L2, and L2 flushed between timed steps"}
 
     if args.impl == "reference":
@@ -223,7 +230,7 @@ def main():
         value = statistics.median(vals)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "int8 QK / fp16 PV (binary16 emulated on CPU)",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "int8 QK / fp16 PV (binary16 emulated on CPU)",
                 "data": "synthetic N(0,1) fp16 (seeded counter RNG), widened to fp32 for the reference",
                 "config": config, "impl": "reference",
                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": kind, "sample": desc},
@@ -349,7 +356,7 @@ def main():
         return
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int8 QK^T (s32 acc) / fp16 PV (fp32 acc); fp16 Q/K/V/O",
         "data": data, "config": config,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * units_total * n * d * 2,

@@ -405,10 +405,14 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     const sab_desc* D = job->desc;
     const size_t in_e = elem_size(D->in_dtype), out_e = elem_size(D->out_dtype);
     const size_t unit_elems = size_t(D->tokens) * D->head_dim;
-    // Chunks of whole units (~96 MB of inputs each) so that H2D of chunk c+1,
-    // compute of chunk c and D2H of chunk c-1 overlap on the three streams.
+    // Chunks of whole units (~24 MB of inputs, and at least ~8 chunks when the
+    // shard allows) so that H2D of chunk c+1, compute of chunk c and D2H of chunk
+    // c-1 overlap on the three streams; small chunks shorten the un-overlapped
+    // first H2D and last D2H.
     const size_t unit_in_bytes = 3 * unit_elems * in_e;
-    const int chunk = int(std::max<size_t>(1, std::min<size_t>(job->count, (96u << 20) / unit_in_bytes)));
+    const size_t by_bytes = std::max<size_t>(1, (24u << 20) / unit_in_bytes);
+    const size_t by_count = std::max<size_t>(1, size_t(job->count) / 8);
+    const int chunk = int(std::max<size_t>(1, std::min<size_t>(job->count, std::min(by_bytes, by_count))));
     const int n_chunks = (job->count + chunk - 1) / chunk;
 
     sab_desc cd = *D;

@@ -52,7 +52,7 @@ __device__ __forceinline__ void load8(const T* src, float (&x)[8]);
 
 template <>
 __device__ __forceinline__ void load8<__half>(const __half* src, float (&x)[8]) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+    const uint4 u = *reinterpret_cast<const uint4*>(src);
     const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -64,8 +64,8 @@ __device__ __forceinline__ void load8<__half>(const __half* src, float (&x)[8]) 
 
 template <>
 __device__ __forceinline__ void load8<float>(const float* src, float (&x)[8]) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(src));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+    const float4 a = *reinterpret_cast<const float4*>(src);
+    const float4 b = *(reinterpret_cast<const float4*>(src) + 1);
     x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
     x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
@@ -244,29 +244,50 @@ __device__ __forceinline__ void int8_scale(float amax, float& delta, float& inv)
     }
 }
 
-// quant.hpp:95-101: clamp(nearbyint(x * inv), -127, 127).
-__device__ __forceinline__ uint32_t code8(float x, float inv) {
-    int c = __float2int_rn(__fmul_rn(x, inv));
-    c = c > 127 ? 127 : (c < -127 ? -127 : c);
-    return static_cast<uint32_t>(c) & 0xFFu;
+// quant.hpp:95-101 on a pair: clamp(nearbyint(x * inv), -127, 127).  The product
+// is rounded first (mul.rn, exactly the reference's `x * inv_scale`), clamped in
+// float (identical to clamping the integer for |v| <= 127.5, and maps +-inf like
+// the reference), and rounded to nearest-even by adding 2^23 + 2^22: the low
+// byte of the biased float's bits is then the two's-complement INT8 code.
+template <bool CLAMP>
+__device__ __forceinline__ uint2 code_pair(float x0, float x1, float inv) {
+    float t0 = __fmul_rn(x0, inv), t1 = __fmul_rn(x1, inv);
+    if (CLAMP) {  // only reachable when 1/delta overflowed (amax < ~127 * 2^-128)
+        t0 = fminf(fmaxf(t0, -127.0f), 127.0f);
+        t1 = fminf(fmaxf(t1, -127.0f), 127.0f);
+    }
+    return make_uint2(__float_as_uint(__fadd_rn(t0, 12582912.0f)), __float_as_uint(__fadd_rn(t1, 12582912.0f)));
 }
 
-__device__ __forceinline__ uint2 codes8(const float (&x)[8], float inv) {
-    uint2 r;
-    r.x = code8(x[0], inv) | (code8(x[1], inv) << 8) | (code8(x[2], inv) << 16) | (code8(x[3], inv) << 24);
-    r.y = code8(x[4], inv) | (code8(x[5], inv) << 8) | (code8(x[6], inv) << 16) | (code8(x[7], inv) << 24);
-    return r;
+// Eight codes packed little-endian into two words (low bytes of the biased floats).
+// Without CLAMP the reference's clamp is a no-op: |x| <= amax gives
+// |x * inv| <= 127 * (1 + 3 ulp) < 127.5 whenever inv = 1/(amax/127) is finite.
+template <bool CLAMP>
+__device__ __forceinline__ uint2 codes8_fast(const float (&x)[8], float inv) {
+    const uint2 a = code_pair<CLAMP>(x[0], x[1], inv), b = code_pair<CLAMP>(x[2], x[3], inv);
+    const uint2 c = code_pair<CLAMP>(x[4], x[5], inv), d = code_pair<CLAMP>(x[6], x[7], inv);
+    const uint32_t lo = __byte_perm(__byte_perm(a.x, a.y, 0x0040), __byte_perm(b.x, b.y, 0x0040), 0x5410);
+    const uint32_t hi = __byte_perm(__byte_perm(c.x, c.y, 0x0040), __byte_perm(d.x, d.y, 0x0040), 0x5410);
+    return make_uint2(lo, hi);
 }
 
-constexpr int kQThreads = 512;
+constexpr int kQThreads = 256;
 
+// One CTA quantizes one 128-token chunk of one unit: the Q and K rows of the
+// chunk (contiguous in HBM) arrive by two bulk copies into shared memory, so
+// the CTA needs few registers and three CTAs share an SM (one's copies overlap
+// another's arithmetic).
 template <typename T, int D>
-__global__ void __launch_bounds__(kQThreads, 1) k1_quantize(PrepassParams p) {
-    constexpr int kThreads = kQThreads;
+__global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
     constexpr int CV = D / 8;
-    constexpr int VPT = kBlockQ * CV / kThreads;  // 8-element vectors per thread per 128-row chunk
+    constexpr int VPT = kBlockQ * CV / kQThreads;  // 8-element vectors per thread per tensor
+    constexpr int kChunkBytes = kBlockQ * D * static_cast<int>(sizeof(T));
+    extern __shared__ __align__(128) uint8_t smem[];
+    T* sq = reinterpret_cast<T*>(smem);
+    T* sk = reinterpret_cast<T*>(smem + kChunkBytes);
+    __shared__ uint64_t bar;
     __shared__ float s_mean[D];
-    __shared__ float s_red[kThreads / 32][3];
+    __shared__ float s_red[kQThreads / 32][3];
     __shared__ float s_inv[3];
 
     const int unit = blockIdx.y;
@@ -275,40 +296,37 @@ __global__ void __launch_bounds__(kQThreads, 1) k1_quantize(PrepassParams p) {
     const int r0 = chunk * kBlockQ;
     const int rows = min(kBlockQ, p.n - r0);
     const size_t ubase = static_cast<size_t>(unit) * p.n * D;
+    const uint32_t bytes = static_cast<uint32_t>(rows) * D * sizeof(T);
 
-    // 1. Issue every Q and K load of this 128-token chunk (kept raw in registers).
-    Raw8<T> qr[VPT], kr[VPT];
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const int v = tid + i * kThreads;
-        const int row = v / CV, col = (v % CV) * 8;
-        if (row < rows) {
-            const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
-            qr[i].load(static_cast<const T*>(p.q) + off);
-            kr[i].load(static_cast<const T*>(p.k) + off);
-        } else {
-            qr[i].zero();
-            kr[i].zero();
-        }
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        fence_barrier_init();
     }
-    // 2. mean_k (computed by k1_mean_final; zero when smoothing is off).
+    __syncthreads();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(smem_u32(&bar), 2 * bytes);
+        bulk_load(smem_u32(sq), static_cast<const T*>(p.q) + ubase + static_cast<size_t>(r0) * D, bytes, smem_u32(&bar));
+        bulk_load(smem_u32(sk), static_cast<const T*>(p.k) + ubase + static_cast<size_t>(r0) * D, bytes, smem_u32(&bar));
+    }
+    // mean_k (computed by k1_mean_final; zero when smoothing is off).
     if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
     __syncthreads();
+    mbar_wait(smem_u32(&bar), 0);
 
-    // 3. fold (Q) / smooth (K) and the group maxima.  Rows past N are excluded.
-    float amax_q = 0.0f, amax_k0 = 0.0f, amax_k1 = 0.0f;
-    bool finite = true;
+    // Pass 1: fold (Q) / smooth (K) in binary32 and the group maxima.
+    float amax_q = 0.0f, amax_k0 = 0.0f, amax_k1 = 0.0f, nan_probe = 0.0f;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-        const int v = tid + i * kThreads;
+        const int v = tid + i * kQThreads;
         const int row = v / CV, col = (v % CV) * 8;
-        float q[8], k[8];
-        qr[i].get(q);
-        kr[i].get(k);
-        finite &= all_finite8(q) && all_finite8(k);
         if (row < rows) {
+            float q[8], k[8];
+            load8<T>(sq + row * D + col, q);
+            load8<T>(sk + row * D + col, k);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
+                nan_probe = fmaf(q[e], 0.0f, nan_probe);  // NaN iff some input is inf or NaN
+                nan_probe = fmaf(k[e], 0.0f, nan_probe);
                 amax_q = fmaxf(amax_q, fabsf(__fmul_rn(q[e], p.fold)));
                 const float ks = fabsf(__fsub_rn(k[e], s_mean[col + e]));
                 if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, ks);
@@ -324,11 +342,11 @@ __global__ void __launch_bounds__(kQThreads, 1) k1_quantize(PrepassParams p) {
         s_red[tid >> 5][1] = amax_k0;
         s_red[tid >> 5][2] = amax_k1;
     }
-    if (!finite) atomicOr(p.status, kStatusNonFinite);
+    if (nan_probe != nan_probe) atomicOr(p.status, kStatusNonFinite);
     __syncthreads();
     if (tid < 3) {
         float m = 0.0f;
-        for (int w = 0; w < kThreads / 32; ++w) m = fmaxf(m, s_red[w][tid]);
+        for (int w = 0; w < kQThreads / 32; ++w) m = fmaxf(m, s_red[w][tid]);
         float delta, inv;
         int8_scale(m, delta, inv);
         s_inv[tid] = inv;
@@ -342,48 +360,46 @@ __global__ void __launch_bounds__(kQThreads, 1) k1_quantize(PrepassParams p) {
     }
     __syncthreads();
 
-    // 4. codes (the binary32 fold / smooth is recomputed from the raw inputs).
+    // Pass 2: codes (the binary32 fold / smooth is recomputed from shared memory).
     const float inv_q = s_inv[0], inv_k0 = s_inv[1], inv_k1 = s_inv[2];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-        const int v = tid + i * kThreads;
+        const int v = tid + i * kQThreads;
         const int row = v / CV, col = (v % CV) * 8;
         if (row < rows) {
             float q[8], k[8];
-            qr[i].get(q);
-            kr[i].get(k);
+            load8<T>(sq + row * D + col, q);
+            load8<T>(sk + row * D + col, k);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 q[e] = __fmul_rn(q[e], p.fold);
                 k[e] = __fsub_rn(k[e], s_mean[col + e]);
             }
             const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
-            *reinterpret_cast<uint2*>(p.qcodes + off) = codes8(q, inv_q);
-            *reinterpret_cast<uint2*>(p.kcodes + off) = codes8(k, i < VPT / 2 ? inv_k0 : inv_k1);
+            const float ik = i < VPT / 2 ? inv_k0 : inv_k1;
+            *reinterpret_cast<uint2*>(p.qcodes + off) =
+                isinf(inv_q) ? codes8_fast<true>(q, inv_q) : codes8_fast<false>(q, inv_q);
+            *reinterpret_cast<uint2*>(p.kcodes + off) = isinf(ik) ? codes8_fast<true>(k, ik) : codes8_fast<false>(k, ik);
         }
     }
 
-    // 5. V: fp32 inputs -> fp16 grid (with the finiteness check); fp16 inputs
-    //    are only scanned when asked (validate_input, attention.hpp:101).
+    // V: fp32 inputs -> fp16 grid (with the finiteness check); fp16 inputs
+    // are only scanned when asked (validate_input, attention.hpp:101).
     if (p.in_f32 || p.check_v) {
         bool vfin = true;
-#pragma unroll
-        for (int i = 0; i < VPT; ++i) {
-            const int v = tid + i * kThreads;
+        for (int v = tid; v < rows * CV; v += kQThreads) {
             const int row = v / CV, col = (v % CV) * 8;
-            if (row < rows) {
-                const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
-                float x[8];
-                load8<T>(static_cast<const T*>(p.v) + off, x);
-                vfin &= all_finite8(x);
-                if (p.in_f32) {
-                    uint4 h;
-                    h.x = pack_half2(x[0], x[1]);
-                    h.y = pack_half2(x[2], x[3]);
-                    h.z = pack_half2(x[4], x[5]);
-                    h.w = pack_half2(x[6], x[7]);
-                    *reinterpret_cast<uint4*>(p.v16 + off) = h;
-                }
+            const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
+            float x[8];
+            load8<T>(static_cast<const T*>(p.v) + off, x);
+            vfin &= all_finite8(x);
+            if (p.in_f32) {
+                uint4 h;
+                h.x = pack_half2(x[0], x[1]);
+                h.y = pack_half2(x[2], x[3]);
+                h.z = pack_half2(x[4], x[5]);
+                h.w = pack_half2(x[6], x[7]);
+                *reinterpret_cast<uint4*>(p.v16 + off) = h;
             }
         }
         if (!vfin) atomicOr(p.status, kStatusNonFinite);
@@ -408,7 +424,10 @@ cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     const dim3 grid((p.n + kBlockQ - 1) / kBlockQ, p.units);
-    k1_quantize<T, D><<<grid, kQThreads, 0, s>>>(p);
+    constexpr int smem = 2 * kBlockQ * D * static_cast<int>(sizeof(T));
+    cudaError_t e = cudaFuncSetAttribute(k1_quantize<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k1_quantize<T, D><<<grid, kQThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 
