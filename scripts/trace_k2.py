@@ -23,7 +23,7 @@ o = torch.empty_like(q)
 ws = sageattn.prepass_cuda(q, k)
 desc = sageattn.make_desc(q, causal, out_dtype=torch.float16)
 ws.desc = desc
-trace = torch.zeros(5 * 512 * 8, dtype=torch.int64, device=dev)
+trace = torch.zeros(19 * 256 * 8, dtype=torch.int64, device=dev)
 lib = _lib.load()
 lib.sab_debug_set_trace.argtypes = [C.c_void_p, C.c_int]
 for it in range(3):
@@ -31,5 +31,5 @@ for it in range(3):
     trace.zero_()
     sageattn.attention_only_cuda(ws, v, o)
     torch.cuda.synchronize()
-np.save(sys.argv[3], trace.cpu().numpy().reshape(5, 512, 8))
+np.save(sys.argv[3], trace.cpu().numpy().reshape(19, 256, 8))
 print("trace saved", sys.argv[3])

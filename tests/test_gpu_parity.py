@@ -119,9 +119,10 @@ def test_attention_within_tolerance(cuda, oracle, shape, causal, dist):
 
 @pytest.mark.parametrize("shape,causal,tiles", [((1, 1, 8192, 128), True, [0, 31, 63]),
                                                 ((1, 1, 17776, 64), False, [0, 70, 138]),
-                                                ((1, 1, 16384, 128), False, [5, 127])])
+                                                ((1, 1, 16384, 128), False, [5, 127]),
+                                                ((1, 1, 131072, 128), True, [0, 3, 40])])  # C5 unit
 def test_attention_sampled_tiles_large(cuda, oracle, shape, causal, tiles):
-    """C2 / C3 / C4 shapes: compare sampled query tiles (units and q-tiles are independent)."""
+    """C2 / C3 / C4 / C5 shapes: compare sampled query tiles (units and q-tiles are independent)."""
     import torch
 
     from paper_2410_02367_b200 import sage_attention_cuda
