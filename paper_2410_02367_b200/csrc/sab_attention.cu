@@ -14,13 +14,17 @@
 // One CTA = one unit x 256 query rows = two 128-row query tiles A and B that
 // share every K^/V tile.  KV tiles are 64 keys = one K quantization group
 // (attention.hpp:345), so each S tile has a single dequant factor.
-// Warp roles (608 threads):
+// Warp roles (576 threads):
 //   warps 0-7  softmax + epilogue of tile A, warps 8-15 of tile B: each warp owns 16
 //              query rows (16 TMEM lanes); threads t and t+16 split a row's 64 keys
 //              (tcgen05.ld 16x32bx2), so 4 softmax warps share each SM sub-partition
-//   warp  16   TMA producer (Q^ of both tiles once; K^ and V per 64-key tile, STAGES-deep ring)
-//   warp  17   MMA issuer of tile A, warp 18 MMA issuer of tile B (whole warp, one elected lane issues):
-//              PV_x(j) once P_x(j) is in TMEM, then QK_x(j+2) into the same S buffer
+//   warp  16   TMA producer (Q^ of both tiles once; K^ and V per 64-key tile on one
+//              barrier, STAGES-deep ring)
+//   warp  17   MMA issuer of both tiles (whole warp, one elected lane issues): per KV tile
+//              j, PV_A(j) once P_A(j) is in TMEM, then QK_A(j+2) into the same S buffer,
+//              then the same for tile B.  Every mbarrier probe sits behind the softmax
+//              warps' MUFU traffic in the SM sub-partition's MIO queue (~250 cycles), so
+//              the issuer keeps the number of waits per KV tile to three.
 // TMEM (512 columns): S_x[b] = [128x + 64b, +64) int32, double-buffered per tile x,
 //                      with P_x(j) stored as fp16x2 over the first 32 columns of
 //                      S_x[j%2] (the A operand of the TMEM-sourced PV MMA);
@@ -31,6 +35,7 @@
 // Rescaling of O is lazy (only when a row max grows by more than 2^8), which is
 // exact in real arithmetic because l and O share the stale max.
 #include <cuda.h>
+#include <algorithm>
 #include <cuda_fp16.h>
 
 #include "sab_internal.h"
@@ -65,16 +70,31 @@ constexpr int kTraceTiles = 512;
 
 constexpr int kBM = 128;
 constexpr int kBN = 64;    // keys per KV tile = one K scale group
-constexpr int kThreads = 608;  // 16 softmax warps + TMA + 2 MMA issuers
+#ifndef SAB_MMA_WARPS
+#define SAB_MMA_WARPS 1
+#endif
+constexpr int kMmaWarps = SAB_MMA_WARPS;  // 1: one issuer for both query tiles; 2: one per tile
+constexpr int kThreads = 544 + 32 * kMmaWarps;  // 16 softmax warps + TMA producer + MMA issuer(s)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
 constexpr int kMaskedAcc = -2147483647;    // sentinel below any reachable INT32 S value
 #ifndef SAB_POLY_PER16
-#define SAB_POLY_PER16 0
+#define SAB_POLY_PER16 2
 #endif
 constexpr int kPolyPer16 = SAB_POLY_PER16;  // exponentials (of 16) evaluated by exp2_poly2 on the FMA pipe
 constexpr float kMagicF = 12582912.0f;     // 2^23 + 2^22
+#ifndef SAB_PIPE
+#define SAB_PIPE 0
+#endif
+// 1: the softmax warp loads S(j+1) before handing P(j) to the MMA issuer.
+constexpr bool kPipe = SAB_PIPE != 0;
+#ifndef SAB_EX2_MODE
+#define SAB_EX2_MODE 0
+#endif
+// 0: ex2.approx.ftz.f32 per element; 1: ex2.approx.f16x2 per pair (input rounded
+// to binary16); 9: no exponential at all (timing experiments only, wrong results).
+constexpr int kEx2Mode = SAB_EX2_MODE;
 
 // ------------------------------------------------------------ packed fp32 math
 struct f2 {
@@ -116,6 +136,17 @@ __device__ __forceinline__ f2 exp2_poly2(f2 x) {
               __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23))};
 }
 
+__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
+    uint32_t y;
+    asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+__device__ __forceinline__ f2 unpack_half2(uint32_t h) {
+    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    return f2{v.x, v.y};
+}
+
 template <int D>
 struct Cfg {
     static constexpr int kStages = D == 128 ? 6 : 8;
@@ -134,7 +165,7 @@ struct Cfg {
 
 struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
     uint64_t q_full;
-    uint64_t k_full[8], k_empty[8], v_full[8], v_empty[8];
+    uint64_t kv_full[8], kv_empty[8];
     uint64_t s_full[2][2], p_full[2][2], pv_done[2], o_final[2];
     uint32_t tmem_base;
 };
@@ -170,7 +201,7 @@ __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
 
 // Softmax of one 64-key S tile row, shared by two threads of a warp: thread t
 // (< 16) holds keys [0, 32) and thread t + 16 keys [32, 64) of TMEM lane t
-// (tcgen05.ld 16x32bx2).  S holds INT32 accumulators of one K scale group with
+// (r, loaded by the caller with tcgen05.ld 16x32bx2).  S holds INT32 accumulators of one K scale group with
 // dequant factor cg = dQ*dK*log2 e.  P is written as fp16x2 over the first 32
 // columns of the same S region (tcgen05.st 16x32bx2: thread t's 16 packed pairs
 // go to columns [16*half, 16*half + 16)), the A operand of the PV MMA.  Updates
@@ -178,13 +209,12 @@ __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
 // O rescale factor (1 when the warp skips the lazy rescale).  `dump` receives
 // the raw half row.
 template <bool MASK, bool CAUSAL>
-__device__ __forceinline__ float softmax_half(uint32_t ts, int half, float cg, int kb, int qi, int n, float& m,
-                                              float& l, bool& rescale, int32_t* dump) {
+__device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t ts, int half, float cg, int kb, int qi,
+                                              int n, float& m, float& l, bool& rescale, int32_t* dump,
+                                              int trole = -1, int ttile = 0) {
     // Keys kb + 32*half + c are valid for c < lim: key < N and, when causal, key <= query.
     const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
-    uint32_t r[32];
-    tmem_ld16x2_32(ts, r);
-    tmem_wait_ld();
+    if (trole >= 0) SAB_STAMP(trole, ttile, 5);
     if (dump) {
 #pragma unroll
         for (int c = 0; c < 32; c += 4) *reinterpret_cast<int4*>(dump + c) = make_int4(r[c], r[c + 1], r[c + 2], r[c + 3]);
@@ -202,6 +232,7 @@ __device__ __forceinline__ float softmax_half(uint32_t ts, int half, float cg, i
         alpha = ex2(m - m_new);
         m = m_new;
     }
+    if (trole >= 0) SAB_STAMP(trole, ttile, 6);
     const float mref = (m == -INFINITY) ? 0.0f : m;
     // p = 2^(float(acc) * cg - m) with float(acc) = bits(acc + 2^23 + 2^22) - (2^23 + 2^22),
     // exact for |acc| < 2^22 (|acc| <= 127^2 * 128 here): one IADD + half an FFMA2 per element.
@@ -216,18 +247,28 @@ __device__ __forceinline__ float softmax_half(uint32_t ts, int half, float cg, i
         const int c = 2 * i;
         const f2 t = ffma2(f2{__uint_as_float(r[c] + kMagicI), __uint_as_float(r[c + 1] + kMagicI)}, cg2, bg);
         f2 pp;
-        if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
-            pp = exp2_poly2(t);
+        if (kEx2Mode == 1) {
+            uint32_t h = ex2_h2(pack_half2(t.x, t.y));
+            if (MASK) h &= ((c >= lim2) ? 0u : 0xFFFFu) | ((c + 1 >= lim2) ? 0u : 0xFFFF0000u);
+            pk[i] = h;
+            pp = unpack_half2(h);
         } else {
-            pp = f2{ex2(t.x), ex2(t.y)};
-        }
-        if (MASK) {
-            pp.x = (c >= lim2) ? 0.0f : pp.x;
-            pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+            if (kEx2Mode == 9) {
+                pp = t;
+            } else if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
+                pp = exp2_poly2(t);
+            } else {
+                pp = f2{ex2(t.x), ex2(t.y)};
+            }
+            if (MASK) {
+                pp.x = (c >= lim2) ? 0.0f : pp.x;
+                pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+            }
+            pk[i] = pack_half2(pp.x, pp.y);
         }
         acc[i & 3] = fadd2(acc[i & 3], pp);
-        pk[i] = pack_half2(pp.x, pp.y);
     }
+    if (trole >= 0) SAB_STAMP(trole, ttile, 7);
     tmem_st16x2_16(ts, pk);
     const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
     l = fmaf(l, alpha, sum.x + sum.y);
@@ -248,7 +289,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sK = smem_u32(smem + C::kOffK);
     const uint32_t sV = smem_u32(smem + C::kOffV);
 
-    const int warp = threadIdx.x / 32;
+    // Warp index through a shuffle so the compiler knows it is warp-uniform: the role
+    // branches below are then uniform and the MMA issuer's loop state lives in
+    // uniform registers (no per-MMA R2UR / election sequences).
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);
     const int lane = threadIdx.x % 32;
     const int n = p.n;
     const int ntq = (n + kBM - 1) / kBM;
@@ -259,9 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (DUMP) {
         unit = p.dump_unit;
         pair = p.dump_qtile / 2;
-    } else {  // longest query-tile pairs first (causal work grows with the pair index)
-        unit = blockIdx.x % p.units;
-        pair = npair - 1 - static_cast<int>(blockIdx.x / p.units);
+    } else {
+        // Raster: units are taken in groups whose K^/V fit in L2 together (group_units,
+        // chosen by the host), so each K^/V tile is fetched from HBM about once and
+        // re-read from L2 by every query-tile pair of its unit.  Inside a group the
+        // longest pairs go first (causal work grows with the pair index).
+        const int gu = p.group_units;
+        const int g = static_cast<int>(blockIdx.x) / (gu * npair);
+        const int r = static_cast<int>(blockIdx.x) - g * gu * npair;
+        const int gsz = min(gu, p.units - g * gu);
+        unit = g * gu + r % gsz;
+        pair = npair - 1 - r / gsz;
     }
     const int qt0 = 2 * pair;
     const bool has_b = qt0 + 1 < ntq;
@@ -273,10 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(smem_u32(&bars->q_full), 1);
         for (int s = 0; s < S; ++s) {
-            mbar_init(smem_u32(&bars->k_full[s]), 1);
-            mbar_init(smem_u32(&bars->k_empty[s]), 2);  // one arrival per MMA issuer
-            mbar_init(smem_u32(&bars->v_full[s]), 1);
-            mbar_init(smem_u32(&bars->v_empty[s]), 2);
+            mbar_init(smem_u32(&bars->kv_full[s]), 1);
+            mbar_init(smem_u32(&bars->kv_empty[s]), kMmaWarps);
         }
         for (int x = 0; x < 2; ++x) {
             for (int b = 0; b < 2; ++b) {
@@ -307,81 +357,87 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = j % S;
                 const uint32_t ph = (j / S) & 1;
                 SAB_STAMP(4, j, 0);
-                mbar_wait(smem_u32(&bars->k_empty[s]), ph ^ 1);
+                mbar_wait(smem_u32(&bars->kv_empty[s]), ph ^ 1);
                 SAB_STAMP(4, j, 1);
-                mbar_arrive_expect_tx(smem_u32(&bars->k_full[s]), C::kKBytes);
-                tma_load_3d(sK + s * C::kKBytes, &tm_k, smem_u32(&bars->k_full[s]), 0, j * kBN, unit);
-                mbar_wait(smem_u32(&bars->v_empty[s]), ph ^ 1);
-                SAB_STAMP(4, j, 2);
-                mbar_arrive_expect_tx(smem_u32(&bars->v_full[s]), C::kVBytes);
+                const uint32_t full = smem_u32(&bars->kv_full[s]);
+                mbar_arrive_expect_tx(full, C::kKBytes + C::kVBytes);
+                tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, j * kBN, unit);
 #pragma unroll
                 for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, smem_u32(&bars->v_full[s]), c * 64,
-                                j * kBN, unit);
+                    tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, j * kBN, unit);
             }
         }
         __syncwarp();
-    } else if (warp == 17 || warp == 18) {
-        // ------------------------------------------------------------ MMA issuer of tile x
-        const int x = warp - 17;
-        const int nkv_x = x == 0 ? nkv_a : nkv_b;
-        {  // the whole warp runs the loop (uniform operands); one elected lane issues
-            constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, kBN);
-            constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
-            // Descriptors are advanced by adding (byte offset >> 4) to the start-address field.
-            const uint64_t dq = make_smem_desc(sQ + x * C::kQBytes, 16, C::kSboQK, C::kSwizzleQK);
-            const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
-            const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
-            const uint32_t t_s0 = tbase + x * 128;
-            const uint32_t t_o = tbase + 256 + x * D;
-            if (nkv_x > 0) mbar_wait(smem_u32(&bars->q_full), 0);
-            tc_fence_after();
-            // QK_x(j) into S_x[j%2].  Issued after PV_x(j-2), which read P_x(j-2) from that
-            // buffer (tcgen05 ops of one thread execute in issue order).
-            auto issue_qk = [&](int j) {
-                const int s = j % S;
-                if (lane == 0) SAB_STAMP(2 + x, j, 0);
-                mbar_wait(smem_u32(&bars->k_full[s]), (j / S) & 1);
-                if (lane == 0) SAB_STAMP(2 + x, j, 1);
-                if (j < nkv_x) {
-                    tc_fence_after();
-                    const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
+    } else if (warp == 17 || (kMmaWarps == 2 && warp == 18)) {
+        // ------------------------------------------------------------ MMA issuer (both tiles)
+        // The whole warp runs the loop (uniform operands); one elected lane issues.  Per KV
+        // tile j: PV_A(j), QK_A(j+2), PV_B(j), QK_B(j+2) -- one K^/V wait per tile for both
+        // query tiles, and the two tiles' softmax phases interleave on the tensor pipe.
+        constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, kBN);
+        constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
+        // Descriptors are advanced by adding (byte offset >> 4) to the start-address field.
+        const uint64_t dq0 = make_smem_desc(sQ, 16, C::kSboQK, C::kSwizzleQK);
+        const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
+        const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
+        if (nkv > 0) mbar_wait(smem_u32(&bars->q_full), 0);
+        // QK_x(j) into S_x[j%2].  Issued after PV_x(j-2), which read P_x(j-2) from that
+        // buffer (tcgen05 ops of one thread execute in issue order).
+        auto issue_qk = [&](int x, int j) {
+            const int s = j % S;
+            const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
+            const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
+            const uint32_t t_s = tbase + x * 128 + (j & 1) * 64;
+            if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 32; ++kk)
-                        umma_i8_ss_w(t_s0 + (j & 1) * 64, dq + static_cast<uint64_t>(kk * 2),
-                                   dk + static_cast<uint64_t>(kk * 2), idesc_qk, kk > 0);
-                    umma_commit_w(smem_u32(&bars->s_full[x][j & 1]));
-                    umma_commit_w(smem_u32(&bars->k_empty[s]));
-                    if (lane == 0) SAB_STAMP(2 + x, j, 2);
-                } else {
-                    mbar_arrive_w(smem_u32(&bars->k_empty[s]));  // tile not used by this query tile
-                }
-            };
-            if (nkv > 0) issue_qk(0);
-            if (nkv > 1) issue_qk(1);
-            for (int j = 0; j < nkv; ++j) {
-                const int s = j % S;
-                mbar_wait(smem_u32(&bars->v_full[s]), (j / S) & 1);
+                for (int kk = 0; kk < D / 32; ++kk)
+                    umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2), idesc_qk,
+                               kk > 0);
+                umma_commit(smem_u32(&bars->s_full[x][j & 1]));
+            }
+            __syncwarp();
+        };
+        auto wait_kv = [&](int j) {
+            if (lane == 0) SAB_STAMP(2, j, 0);
+            mbar_wait(smem_u32(&bars->kv_full[j % S]), (j / S) & 1);
+            tc_fence_after();
+            if (lane == 0) SAB_STAMP(2, j, 1);
+        };
+        const int x_lo = kMmaWarps == 2 ? warp - 17 : 0;
+        const int x_hi = kMmaWarps == 2 ? warp - 17 : 1;
+        for (int j = 0; j < 2 && j < nkv; ++j) {
+            wait_kv(j);
+            if (j < nkv_a && x_lo == 0) issue_qk(0, j);
+            if (j < nkv_b && x_hi == 1) issue_qk(1, j);
+        }
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j % S;
+            const bool next = j + 2 < nkv;
+            if (next) wait_kv(j + 2);
+            for (int x = x_lo; x <= x_hi; ++x) {
+                const int nkv_x = x == 0 ? nkv_a : nkv_b;
                 if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
                     if (lane == 0) SAB_STAMP(2 + x, j, 3);
                     mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
-                    if (lane == 0) SAB_STAMP(2 + x, j, 4);
                     tc_fence_after();
+                    if (lane == 0) SAB_STAMP(2 + x, j, 4);
                     const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
-                    const uint32_t t_p = t_s0 + (j & 1) * 64;
+                    const uint32_t t_p = tbase + x * 128 + (j & 1) * 64;
+                    const uint32_t t_o = tbase + 256 + x * D;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < kBN / 16; ++kk)
-                        umma_f16_ts_w(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
-                                    (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit_w(smem_u32(&bars->pv_done[x]));
-                    umma_commit_w(smem_u32(&bars->v_empty[s]));
-                    if (j == nkv_x - 1) umma_commit_w(smem_u32(&bars->o_final[x]));
+                        for (int kk = 0; kk < kBN / 16; ++kk)
+                            umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
+                                        (j > 0 || kk > 0) ? 1u : 0u);
+                        umma_commit(smem_u32(&bars->pv_done[x]));
+                        if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
+                    }
+                    __syncwarp();
                     if (lane == 0) SAB_STAMP(2 + x, j, 5);
-                } else {
-                    mbar_arrive_w(smem_u32(&bars->v_empty[s]));
                 }
-                if (j + 2 < nkv) issue_qk(j + 2);
+                if (next && j + 2 < nkv_x) issue_qk(x, j + 2);
             }
+            if (elect_one()) umma_commit(smem_u32(&bars->kv_empty[s]));  // K^(j), V(j) free once these MMAs finish
+            __syncwarp();
         }
         __syncwarp();
     } else if (warp < 16) {
@@ -403,14 +459,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* ksc = p.kscales + static_cast<size_t>(unit) * ntk;
             // The K scale of the next KV tile is fetched one iteration ahead.
             float ks_next = __ldg(ksc);
+            const bool tr = (warp % 8) == 0 && lane == 0;
+            // Software pipeline: S(j+1) is loaded from TMEM while P(j) is stored and
+            // handed to the MMA issuer, so the load latency is off the per-tile chain.
+            uint32_t r[32];
+            if (tr) SAB_STAMP(x, 0, 0);
+            mbar_wait(smem_u32(&bars->s_full[x][0]), 0);
+            tc_fence_after();
+            tmem_ld16x2_32(tbase + lane_off + x * 128, r);
             for (int j = 0; j < nkv_x; ++j) {
                 const float ks_cur = ks_next;
                 if (j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
                 const int b = j & 1;
-                const bool tr = (warp % 8) == 0 && lane == 0;
-                if (tr) SAB_STAMP(x, j, 0);
-                mbar_wait(smem_u32(&bars->s_full[x][b]), (j >> 1) & 1);
-                tc_fence_after();
+                tmem_wait_ld_dep(r);
                 if (tr) SAB_STAMP(x, j, 1);
                 const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
                 int32_t* dump = (DUMP && qt == p.dump_qtile)
@@ -423,10 +484,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool rescale;
                 float alpha;
                 if (need_mask)
-                    alpha = softmax_half<true, CAUSAL>(t_s, half, cg, kb, qi, n, m, l, rescale, dump);
+                    alpha = softmax_half<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
                 else
-                    alpha = softmax_half<false, CAUSAL>(t_s, half, cg, kb, qi, n, m, l, rescale, dump);
+                    alpha = softmax_half<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
                 if (tr) SAB_STAMP(x, j, 2);
+                if (kPipe && j + 1 < nkv_x) {
+                    if (tr) SAB_STAMP(x, j + 1, 0);
+                    mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((j + 1) >> 1) & 1);
+                    tc_fence_after();
+                    tmem_ld16x2_32(tbase + lane_off + x * 128 + (b ^ 1) * 64, r);
+                }
                 if (rescale && j > 0) {
                     // O_x must hold P(j-1)V(j-1) before it is rescaled.  PV_x(j-2) is complete
                     // (QK_x(j) was issued after it), so parity (j-1)&1 of pv_done is unambiguous.
@@ -449,6 +516,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));  // one arrival per warp
                 if (tr) SAB_STAMP(x, j, 4);
+                if (!kPipe && j + 1 < nkv_x) {
+                    if (tr) SAB_STAMP(x, j + 1, 0);
+                    mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((j + 1) >> 1) & 1);
+                    tc_fence_after();
+                    tmem_ld16x2_32(tbase + lane_off + x * 128 + (b ^ 1) * 64, r);
+                }
             }
 
             // -------------------------------------------------------- epilogue
@@ -538,6 +611,13 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
         !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBN, swqk) ||
         !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, kBN, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
+    // Raster groups: as few groups as keep each group's K^ (int8) and V (fp16) within
+    // ~96 MB of the 126 MB L2, balanced in size.
+    AttnParams pp = p;
+    const size_t kv_unit = static_cast<size_t>(p.n) * D * 3;
+    const size_t per_group = std::max<size_t>(1, (96u << 20) / kv_unit);
+    const size_t groups = (static_cast<size_t>(p.units) + per_group - 1) / per_group;
+    pp.group_units = static_cast<int>((static_cast<size_t>(p.units) + groups - 1) / groups);
     auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -547,7 +627,7 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     cudaMemcpyToSymbolAsync(g_trace, &h_trace_ptr, sizeof(h_trace_ptr), 0, cudaMemcpyHostToDevice, s);
     cudaMemcpyToSymbolAsync(g_trace_cta, &h_trace_cta, sizeof(int), 0, cudaMemcpyHostToDevice, s);
 #endif
-    kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, p);
+    kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, pp);
     return cudaGetLastError();
 }
 

@@ -58,6 +58,7 @@ struct AttnParams {
     int32_t* s_dump;  // debug: INT32 S tiles of one (unit, q-tile)
     int units, n, d, causal, out_f32;
     int dump_unit, dump_qtile;
+    int group_units;  // K2 raster: units per L2-resident group (set by launch_attention)
 };
 
 cudaError_t launch_attention(const AttnParams& p, cudaStream_t s);

@@ -59,19 +59,40 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 }
 
 // Blocks until the phase with parity `parity` of the barrier has completed.
-// A non-blocking test_wait handles the common already-complete case cheaply;
-// otherwise try_wait with a suspend-time hint parks the warp instead of
-// re-issuing the loop, so waiting warps do not steal issue slots from the
-// softmax warps sharing their SM sub-partition.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    if (mbar_test(bar, parity)) return;
+// try_wait without a suspend-time hint (SYNCS.PHASECHK.TRANS64.TRYWAIT): ~90
+// cycles when the phase is already complete, a hardware sleep with ~60-cycle
+// wake-up otherwise.
+__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "SAB_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra SAB_WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+
+// Same, but a waiter that finds the phase incomplete is parked (try_wait with a
+// suspend-time hint -> NANOSLEEP.SYNCS) instead of re-issuing the probe, so it
+// does not take issue / MIO slots from the warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    if (mbar_test(bar, parity)) return;
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SAB_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra SAB_WAITS_%=;\n\t}" ::"r"(bar),
         "r"(parity), "r"(0x989680)
         : "memory");
+}
+
+#ifndef SAB_WAIT_SLEEP
+#define SAB_WAIT_SLEEP 1
+#endif
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    if (SAB_WAIT_SLEEP) mbar_wait_sleep(bar, parity);
+    else mbar_wait_spin(bar, parity);
 }
 
 // --------------------------------------------------------------------- TMA
@@ -156,6 +177,17 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                  : "memory");
 }
 
+// True in exactly one lane of the converged warp (elect.sync).  Used as
+// `if (elect_one()) { ...tcgen05 issue... }` so a warp-uniform loop issues each
+// single-thread tcgen05 op once, with its operands in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // Warp-wide variants: the whole (converged) warp executes them with warp-uniform
 // operands and one elected lane issues, so the descriptors live in uniform
 // registers and no per-instruction election loop is generated.
@@ -199,6 +231,20 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// tcgen05.wait::ld that also ties the 32 destination registers of an earlier
+// (software-pipelined) tcgen05.ld to this point, so the compiler cannot move
+// their consumers above the wait.
+__device__ __forceinline__ void tmem_wait_ld_dep(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
 
 // 32 lanes x 32 consecutive 32-bit columns: thread t gets columns [0,32) of lane t.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
