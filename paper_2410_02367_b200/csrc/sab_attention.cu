@@ -5,7 +5,7 @@
 //   s = (float(acc) * dQ) * dK (409-414)    -> one FFMA per element with dQ*dK*log2(e) (exp2 domain)
 //   causal tile classes (79-94, 399-427)    -> fully masked KV tiles are never issued; the element
 //                                              mask runs only on the diagonal / ragged tail tile
-//   online softmax (429-443)                -> registers, one thread per query row
+//   online softmax (429-443)                -> registers, two threads per query row
 //   P~ V with binary16 operands (447-475)   -> P packed to fp16 into TMEM (aliasing S),
 //                                              tcgen05.mma kind::f16 with A from TMEM, V from SMEM,
 //                                              FP32 accumulator in TMEM (the pv_fp32_accumulator arm)
@@ -18,14 +18,18 @@
 //   warps 0-7  softmax + epilogue of tile A, warps 8-15 of tile B: each warp owns 16
 //              query rows (16 TMEM lanes); threads t and t+16 split a row's 64 keys
 //              (tcgen05.ld 16x32bx2), so 4 softmax warps share each SM sub-partition
+//              (the exponentials are latency-bound at 2 warps per sub-partition and
+//              MUFU-bound at 4; see scripts/micro/softmax_row.cu)
 //   warp  16   TMA producer (Q^ of both tiles once; K^ and V per 64-key tile on one
 //              barrier, STAGES-deep ring)
-//   warp  17   MMA issuer of both tiles (whole warp, one elected lane issues): per KV tile
-//              j, PV_A(j) once P_A(j) is in TMEM, then QK_A(j+2) into the same S buffer,
-//              then the same for tile B.  Every mbarrier probe sits behind the softmax
-//              warps' MUFU traffic in the SM sub-partition's MIO queue (~250 cycles), so
-//              the issuer keeps the number of waits per KV tile to three.
-// TMEM (512 columns): S_x[b] = [128x + 64b, +64) int32, double-buffered per tile x,
+//   warp  17   MMA issuer of both tiles (warp-uniform loop in uniform registers, one
+//              elected lane issues): per KV tile j, PV_A(j) once P_A(j) is in TMEM, then
+//              bias + QK_A(j+2) into the same S buffer, then the same for tile B.
+// S bias: each S tile starts with one kind::f16 MMA of constant operands that writes
+// the binary32 value 2^23 + 2^22 (bits 0x4B400000) into every accumulator; the
+// kind::i8 MMAs then accumulate INT32 products onto those bits, so the softmax reads
+// float(2^23 + 2^22 + acc) with no per-element integer-to-float conversion.
+// TMEM (512 columns): S_x[b] = [128x + 64b, +64), double-buffered per tile x,
 //                      with P_x(j) stored as fp16x2 over the first 32 columns of
 //                      S_x[j%2] (the A operand of the TMEM-sourced PV MMA);
 //                      O_A [256, 256+D), O_B [256+D, 256+2D) fp32 accumulators.
@@ -70,31 +74,16 @@ constexpr int kTraceTiles = 512;
 
 constexpr int kBM = 128;
 constexpr int kBN = 64;    // keys per KV tile = one K scale group
-#ifndef SAB_MMA_WARPS
-#define SAB_MMA_WARPS 1
-#endif
-constexpr int kMmaWarps = SAB_MMA_WARPS;  // 1: one issuer for both query tiles; 2: one per tile
-constexpr int kThreads = 544 + 32 * kMmaWarps;  // 16 softmax warps + TMA producer + MMA issuer(s)
+constexpr int kThreads = 576;  // 16 softmax warps + TMA producer + MMA issuer
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
-constexpr int kMaskedAcc = -2147483647;    // sentinel below any reachable INT32 S value
+constexpr int kMaskedAcc = 0;              // sentinel below any biased S value (bits of +0.0f)
 #ifndef SAB_POLY_PER16
 #define SAB_POLY_PER16 2
 #endif
 constexpr int kPolyPer16 = SAB_POLY_PER16;  // exponentials (of 16) evaluated by exp2_poly2 on the FMA pipe
 constexpr float kMagicF = 12582912.0f;     // 2^23 + 2^22
-#ifndef SAB_PIPE
-#define SAB_PIPE 0
-#endif
-// 1: the softmax warp loads S(j+1) before handing P(j) to the MMA issuer.
-constexpr bool kPipe = SAB_PIPE != 0;
-#ifndef SAB_EX2_MODE
-#define SAB_EX2_MODE 0
-#endif
-// 0: ex2.approx.ftz.f32 per element; 1: ex2.approx.f16x2 per pair (input rounded
-// to binary16); 9: no exponential at all (timing experiments only, wrong results).
-constexpr int kEx2Mode = SAB_EX2_MODE;
 
 // ------------------------------------------------------------ packed fp32 math
 struct f2 {
@@ -136,17 +125,6 @@ __device__ __forceinline__ f2 exp2_poly2(f2 x) {
               __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23))};
 }
 
-__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
-    uint32_t y;
-    asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
-}
-
-__device__ __forceinline__ f2 unpack_half2(uint32_t h) {
-    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&h));
-    return f2{v.x, v.y};
-}
-
 template <int D>
 struct Cfg {
     static constexpr int kStages = D == 128 ? 6 : 8;
@@ -159,7 +137,10 @@ struct Cfg {
     static constexpr int kOffQ = 0;
     static constexpr int kOffK = kOffQ + 2 * kQBytes;
     static constexpr int kOffV = kOffK + kStages * kKBytes;
-    static constexpr int kOffBar = kOffV + kStages * kVBytes;
+    // Constant fp16 operands of the bias MMA (A: 2048, B: 384; 16 * 2048 * 384 = 2^23 + 2^22).
+    static constexpr int kOffBiasA = kOffV + kStages * kVBytes;
+    static constexpr int kOffBiasB = kOffBiasA + 8192;
+    static constexpr int kOffBar = kOffBiasB + 4096;
     static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // barriers + alignment slack
 };
 
@@ -178,8 +159,9 @@ __device__ __forceinline__ int opaque(int v) {
     return r;
 }
 
-// Max of N INT32 accumulators: 4 independent chains.  With MASK, columns
-// >= lim are excluded.
+// Max of N biased S accumulators as integers (2^23 + 2^22 + acc: positive
+// binary32 values, ordered like their bit patterns): 4 independent chains.
+// With MASK, columns >= lim are excluded.
 template <bool MASK, int N>
 __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
     int mi[4];
@@ -217,14 +199,16 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
     if (trole >= 0) SAB_STAMP(trole, ttile, 5);
     if (dump) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 4) *reinterpret_cast<int4*>(dump + c) = make_int4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+        for (int c = 0; c < 32; c += 4)  // the raw INT32 accumulators (bias removed)
+            *reinterpret_cast<int4*>(dump + c) = make_int4(r[c] - kMagicI, r[c + 1] - kMagicI, r[c + 2] - kMagicI,
+                                                           r[c + 3] - kMagicI);
     }
     // Row max on the INT32 accumulators: acc -> acc*cg is monotone for cg > 0, so
     // this is the reference's binary32 row max (attention.hpp:431-432) up to the
     // final scaling.  The two halves of a row meet by a shuffle.
     int imax = group_max<MASK>(r, lim);
     imax = max(imax, __shfl_xor_sync(0xffffffffu, imax, 16));
-    const float mx = (MASK && imax == kMaskedAcc) ? -INFINITY : static_cast<float>(imax) * cg;
+    const float mx = (MASK && imax == kMaskedAcc) ? -INFINITY : (__int_as_float(imax) - kMagicF) * cg;
     const float m_new = fmaxf(m, mx);
     rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
     float alpha = 1.0f;
@@ -234,8 +218,10 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
     }
     if (trole >= 0) SAB_STAMP(trole, ttile, 6);
     const float mref = (m == -INFINITY) ? 0.0f : m;
-    // p = 2^(float(acc) * cg - m) with float(acc) = bits(acc + 2^23 + 2^22) - (2^23 + 2^22),
-    // exact for |acc| < 2^22 (|acc| <= 127^2 * 128 here): one IADD + half an FFMA2 per element.
+    // p = 2^(float(acc) * cg - m).  The S accumulators arrive biased: their bits are
+    // bits(2^23 + 2^22) + acc (the bias MMA, see k2_attention), i.e. the binary32 value
+    // 2^23 + 2^22 + acc exactly for |acc| < 2^22 (|acc| <= 127^2 * 128 here), so
+    // float(acc) * cg - m is half an FFMA2 per element with no conversion.
     const f2 cg2{cg, cg};
     const float bgs = -fmaf(kMagicF, cg, mref);
     const f2 bg{bgs, bgs};
@@ -245,27 +231,18 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const int c = 2 * i;
-        const f2 t = ffma2(f2{__uint_as_float(r[c] + kMagicI), __uint_as_float(r[c + 1] + kMagicI)}, cg2, bg);
+        const f2 t = ffma2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, cg2, bg);
         f2 pp;
-        if (kEx2Mode == 1) {
-            uint32_t h = ex2_h2(pack_half2(t.x, t.y));
-            if (MASK) h &= ((c >= lim2) ? 0u : 0xFFFFu) | ((c + 1 >= lim2) ? 0u : 0xFFFF0000u);
-            pk[i] = h;
-            pp = unpack_half2(h);
+        if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
+            pp = exp2_poly2(t);
         } else {
-            if (kEx2Mode == 9) {
-                pp = t;
-            } else if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
-                pp = exp2_poly2(t);
-            } else {
-                pp = f2{ex2(t.x), ex2(t.y)};
-            }
-            if (MASK) {
-                pp.x = (c >= lim2) ? 0.0f : pp.x;
-                pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
-            }
-            pk[i] = pack_half2(pp.x, pp.y);
+            pp = f2{ex2(t.x), ex2(t.y)};
         }
+        if (MASK) {
+            pp.x = (c >= lim2) ? 0.0f : pp.x;
+            pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+        }
+        pk[i] = pack_half2(pp.x, pp.y);
         acc[i & 3] = fadd2(acc[i & 3], pp);
     }
     if (trole >= 0) SAB_STAMP(trole, ttile, 7);
@@ -322,11 +299,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nkv_b = has_b ? (CAUSAL ? min(2 * qt0 + 4, ntk) : ntk) : 0;
     const int nkv = max(nkv_a, nkv_b);
 
+    {  // constant operands of the bias MMA, written once through the generic proxy
+        uint4* bias = reinterpret_cast<uint4*>(smem + C::kOffBiasA);
+        const uint4 a2048 = make_uint4(0x68006800u, 0x68006800u, 0x68006800u, 0x68006800u);
+        const uint4 b384 = make_uint4(0x5E005E00u, 0x5E005E00u, 0x5E005E00u, 0x5E005E00u);
+        for (int i = threadIdx.x; i < (8192 + 4096) / 16; i += kThreads) bias[i] = i < 8192 / 16 ? a2048 : b384;
+        fence_proxy_async_smem();  // visible to the tensor core (async proxy)
+    }
     if (threadIdx.x == 0) {
         mbar_init(smem_u32(&bars->q_full), 1);
         for (int s = 0; s < S; ++s) {
             mbar_init(smem_u32(&bars->kv_full[s]), 1);
-            mbar_init(smem_u32(&bars->kv_empty[s]), kMmaWarps);
+            mbar_init(smem_u32(&bars->kv_empty[s]), 1);
         }
         for (int x = 0; x < 2; ++x) {
             for (int b = 0; b < 2; ++b) {
@@ -368,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 17 || (kMmaWarps == 2 && warp == 18)) {
+    } else if (warp == 17) {
         // ------------------------------------------------------------ MMA issuer (both tiles)
         // The whole warp runs the loop (uniform operands); one elected lane issues.  Per KV
         // tile j: PV_A(j), QK_A(j+2), PV_B(j), QK_B(j+2) -- one K^/V wait per tile for both
@@ -379,6 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dq0 = make_smem_desc(sQ, 16, C::kSboQK, C::kSwizzleQK);
         const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
         const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
+        constexpr uint32_t idesc_bias = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 0, kBM, kBN);
+        const uint64_t d_bias_a = make_smem_desc(smem_u32(smem + C::kOffBiasA), 128, 256, kSwizzleNone);
+        const uint64_t d_bias_b = make_smem_desc(smem_u32(smem + C::kOffBiasB), 128, 256, kSwizzleNone);
         if (nkv > 0) mbar_wait(smem_u32(&bars->q_full), 0);
         // QK_x(j) into S_x[j%2].  Issued after PV_x(j-2), which read P_x(j-2) from that
         // buffer (tcgen05 ops of one thread execute in issue order).
@@ -388,10 +375,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
             const uint32_t t_s = tbase + x * 128 + (j & 1) * 64;
             if (elect_one()) {
+                // Bias MMA: S = 2^23 + 2^22 as binary32 (bits 0x4B400000) from constant fp16
+                // operands, then the INT32 QK^T products accumulate onto those bits, so the
+                // softmax reads float(2^23 + 2^22 + acc) directly.
+                umma_f16_ss(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
 #pragma unroll
                 for (int kk = 0; kk < D / 32; ++kk)
                     umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2), idesc_qk,
-                               kk > 0);
+                               1u);
                 umma_commit(smem_u32(&bars->s_full[x][j & 1]));
             }
             __syncwarp();
@@ -402,18 +393,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (lane == 0) SAB_STAMP(2, j, 1);
         };
-        const int x_lo = kMmaWarps == 2 ? warp - 17 : 0;
-        const int x_hi = kMmaWarps == 2 ? warp - 17 : 1;
         for (int j = 0; j < 2 && j < nkv; ++j) {
             wait_kv(j);
-            if (j < nkv_a && x_lo == 0) issue_qk(0, j);
-            if (j < nkv_b && x_hi == 1) issue_qk(1, j);
+            if (j < nkv_a) issue_qk(0, j);
+            if (j < nkv_b) issue_qk(1, j);
         }
         for (int j = 0; j < nkv; ++j) {
             const int s = j % S;
             const bool next = j + 2 < nkv;
             if (next) wait_kv(j + 2);
-            for (int x = x_lo; x <= x_hi; ++x) {
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
                 const int nkv_x = x == 0 ? nkv_a : nkv_b;
                 if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
                     if (lane == 0) SAB_STAMP(2 + x, j, 3);
@@ -488,12 +478,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                     alpha = softmax_half<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
                 if (tr) SAB_STAMP(x, j, 2);
-                if (kPipe && j + 1 < nkv_x) {
-                    if (tr) SAB_STAMP(x, j + 1, 0);
-                    mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((j + 1) >> 1) & 1);
-                    tc_fence_after();
-                    tmem_ld16x2_32(tbase + lane_off + x * 128 + (b ^ 1) * 64, r);
-                }
                 if (rescale && j > 0) {
                     // O_x must hold P(j-1)V(j-1) before it is rescaled.  PV_x(j-2) is complete
                     // (QK_x(j) was issued after it), so parity (j-1)&1 of pv_done is unambiguous.
@@ -516,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));  // one arrival per warp
                 if (tr) SAB_STAMP(x, j, 4);
-                if (!kPipe && j + 1 < nkv_x) {
+                if (j + 1 < nkv_x) {  // S(j+1) is issued into TMEM registers now; waited at the loop top
                     if (tr) SAB_STAMP(x, j + 1, 0);
                     mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((j + 1) >> 1) & 1);
                     tc_fence_after();

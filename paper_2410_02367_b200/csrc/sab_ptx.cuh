@@ -87,13 +87,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
-#ifndef SAB_WAIT_SLEEP
-#define SAB_WAIT_SLEEP 1
-#endif
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    if (SAB_WAIT_SLEEP) mbar_wait_sleep(bar, parity);
-    else mbar_wait_spin(bar, parity);
-}
+// Default wait: parking the waiter measured faster than spinning (the softmax warps
+// are issue-bound, and a spinning waiter takes their issue / MIO slots).
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) { mbar_wait_sleep(bar, parity); }
 
 // --------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
