@@ -72,13 +72,13 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """NVML sampler (every 20 ms) of SM clock and throttle reasons while the GPU is busy."""
+    """NVML sampler (every 2 ms) of SM clock, power and throttle reasons during the timed region."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
                0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.power, self.reasons, self.max_mhz, self.limit_w = [], [], set(), None, None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -87,6 +87,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:  # noqa: BLE001
+                self.limit_w = None
         except Exception:  # noqa: BLE001 - clocks are reported as unavailable
             self.nv = None
         self.t = threading.Thread(target=self._run, daemon=True)
@@ -94,17 +98,16 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                if util > 0:
-                    self.samples.append(mhz)
-                    for bit, name in self.REASONS.items():
-                        if r & bit:
-                            self.reasons.add(name)
+                self.samples.append(mhz)
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nv:
@@ -120,7 +123,10 @@ class ClockSampler:
         if not self.nv:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "sm_min_mhz": min(self.samples) if self.samples else None,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power) if self.power else None,
+                "power_limit_w": self.limit_w}
 
 
 # ----------------------------------------------------------------------------- CPU reference sample
@@ -295,20 +301,22 @@ def main():
 
     sampler = ClockSampler(dev.index)
     t_step, t_k1, t_k2 = [], [], []
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     with sampler:
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        for _ in range(args.steps):
+        for i in range(args.steps):
             flush.fill_(2)  # evict the previous step's data from L2 (outside the timed events)
+            ev = evs[i]
             ev[0].record(stream)
             step()
             ev[2].record(stream)
-            ev[2].synchronize()
+        torch.cuda.synchronize()
+        for ev in evs:
             t_step.append(ev[0].elapsed_time(ev[2]))
             t_k1.append(ev[0].elapsed_time(ev[1]))
             t_k2.append(ev[1].elapsed_time(ev[2]))
-        torch.cuda.synchronize()
         if dist:
             dist.barrier()
 
@@ -362,7 +370,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * units_total * n * d * 2,
                 "d2h_bytes_per_step": units_total * n * d * 2,
                 "how": "sab_attention_fwd_host on pinned host buffers, wall clock, max over ranks"},
-        "gpu_launches": args.steps * 4,  # k1_mean_partials + k1_mean_final + k1_quantize + k2_attention
+        "gpu_launches": args.steps * 3,  # k1_mean_partials (+ fused tree top) + k1_quantize + k2_attention
         "roofline": {"bound": "tensor", "achieved": k2_ach, "peak": p_mix, "unit": "TFLOP/s",
                      "frac": k2_ach / p_mix, "traffic": traffic, "kernel": "k2_attention",
                      "ms_per_launch": k2_mean_ms,

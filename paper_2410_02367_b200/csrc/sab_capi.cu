@@ -58,7 +58,7 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     L->mean_k = take(units * hd * sizeof(float));
     L->partials = take(units * size_t(n_partials) * hd * sizeof(float));
     L->v16 = take(d->in_dtype == SAB_F32 ? units * n * hd * 2 : 0);
-    L->status = take(sizeof(int32_t));
+    L->status = take(sizeof(int32_t) * (1 + units));  // status word + per-unit K1 counters
     L->total = off;
     L->n_partials = n_partials;
     L->tree_depth = depth;
@@ -84,6 +84,7 @@ PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const vo
     p.partials = at<float>(ws, L.partials);
     p.v16 = d->in_dtype == SAB_F32 ? at<uint16_t>(ws, L.v16) : nullptr;
     p.status = at<int>(ws, L.status);
+    p.counters = p.status + 1;
     p.units = int(units_of(d));
     p.n = d->tokens;
     p.d = d->head_dim;
@@ -121,7 +122,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 int enqueue_prepass(const sab_desc* d, const sab_ws_layout& L, const void* q, const void* k, const void* v, void* ws,
                     cudaStream_t s, bool reset) {
     if (reset) {
-        cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t), s);
+        cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t) * (1 + size_t(units_of(d))), s);
         if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: status reset");
     }
     cudaError_t e = launch_prepass(prepass_params(d, L, q, k, v, ws), s);
@@ -431,7 +432,7 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     uint8_t* dout = dv + in_bytes;
     uint8_t* ws = dout + out_bytes;
 
-    if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t), ctx->s_cmp)) != cudaSuccess)
+    if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t) * (1 + size_t(chunk)), ctx->s_cmp)) != cudaSuccess)
         return cuda_fail(e, "sab_attention_fwd_host: memset");
     int st = SAB_OK;
     for (int c = 0; c < n_chunks && st == SAB_OK; ++c) {

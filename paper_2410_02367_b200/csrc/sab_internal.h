@@ -29,6 +29,7 @@ struct PrepassParams {
     float* partials;
     uint16_t* v16;
     int* status;
+    int* counters;      // per unit: mean-partial CTAs done (self-resetting, zeroed with status)
     int units, n, d;
     int depth;          // tree depth of the 4..9-token node level
     int nodes_per_cta;  // nodes summed per mean-partial CTA (power of two)

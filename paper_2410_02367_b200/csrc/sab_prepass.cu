@@ -7,12 +7,12 @@
 //   V -> binary16 grid  attention.hpp:371-375 (fp32 inputs only; F9: hardware
 //                       cvt.rn.f16.f32 == round_to_half for finite floats)
 //
-// Three launches per call:
+// Two launches per call:
 //   k1_mean_partials  grid (n_partials, units): each CTA sums an aligned
 //                     subtree of 'nodes_per_cta' leaf-level nodes of the
-//                     reference's pairwise tree for all head_dim channels.
-//   k1_mean_final     grid (units): the top of the same tree over the CTA
-//                     partials -> mean_k (bit-exact).
+//                     reference's pairwise tree for all head_dim channels;
+//                     the last CTA of each unit (per-unit counter) then sums
+//                     the top of the tree over the CTA partials -> mean_k.
 //   k1_quantize       grid (ceil(N/128), units): reads mean_k, then quantizes
 //                     one 128-token Q group and the two 64-token K groups of
 //                     that chunk.
@@ -26,6 +26,8 @@
 // No fast-math anywhere: explicit __fmul_rn / __fsub_rn / __fdiv_rn /
 // __float2int_rn reproduce the reference's binary32 operations one for one.
 #include <cuda_fp16.h>
+
+#include <type_traits>
 
 #include "sab_internal.h"
 #include "sab_ptx.cuh"
@@ -143,6 +145,32 @@ __device__ __forceinline__ void seq_sum(const T* base, int t0, int t1, int col, 
     }
 }
 
+// Top of the pairwise tree: combines the n_partials (power of two) CTA partial
+// sums of one unit as a perfect binary tree (binary-counter evaluation, left +
+// right), then mean = sum * (1.0f / N)  (quant.hpp:228, 235).  Channel c; the
+// partials of the other CTAs are read through L2 (__ldcg).
+template <int D>
+__device__ __forceinline__ void mean_top(const PrepassParams& p, int unit, int c) {
+    const float* part = p.partials + static_cast<size_t>(unit) * p.n_partials * D + c;
+    float stk[24];
+    int top = 0;
+    for (int i0 = 0; i0 < p.n_partials; i0 += 8) {  // n_partials is 1, 2, 4 or a multiple of 8
+        float xs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xs[u] = (i0 + u < p.n_partials) ? __ldcg(part + static_cast<size_t>(i0 + u) * D) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u;
+            if (i < p.n_partials) {
+                float x = xs[u];
+                for (int t = i; t & 1; t >>= 1) x = __fadd_rn(stk[--top], x);
+                stk[top++] = x;
+            }
+        }
+    }
+    p.mean[static_cast<size_t>(unit) * D + c] = __fmul_rn(stk[0], p.inv_n);
+}
+
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
     constexpr int CV = D / 8;           // 8-channel vectors per row
@@ -199,32 +227,19 @@ __global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) dst[i] = red[0][cv * 8 + i];
     }
-}
-
-// Top of the pairwise tree: combines the n_partials (power of two) CTA partial
-// sums of one unit as a perfect binary tree (binary-counter evaluation, left +
-// right), then mean = sum * (1.0f / N)  (quant.hpp:228, 235).
-template <int D>
-__global__ void __launch_bounds__(D) k1_mean_final(PrepassParams p) {
-    const int unit = blockIdx.x, c = threadIdx.x;
-    const float* part = p.partials + static_cast<size_t>(unit) * p.n_partials * D + c;
-    float stk[24];
-    int top = 0;
-    for (int i0 = 0; i0 < p.n_partials; i0 += 8) {  // n_partials is 1, 2, 4 or a multiple of 8
-        float xs[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) xs[u] = (i0 + u < p.n_partials) ? part[static_cast<size_t>(i0 + u) * D] : 0.0f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u;
-            if (i < p.n_partials) {
-                float x = xs[u];
-                for (int t = i; t & 1; t >>= 1) x = __fadd_rn(stk[--top], x);
-                stk[top++] = x;
-            }
-        }
+    // The last CTA of the unit to finish sums the top of the tree (no second launch).
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_last = atomicAdd(p.counters + unit, 1) == p.n_partials - 1;
+        if (s_last) p.counters[unit] = 0;  // ready for the next call
     }
-    p.mean[static_cast<size_t>(unit) * D + c] = __fmul_rn(stk[0], p.inv_n);
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (threadIdx.x < D) mean_top<D>(p, unit, threadIdx.x);
+    }
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -271,6 +286,52 @@ __device__ __forceinline__ uint2 codes8_fast(const float (&x)[8], float inv) {
     return make_uint2(lo, hi);
 }
 
+// ---- packed helpers for the fp16 fast path (two binary32 lanes per instruction)
+struct f2 {
+    float x, y;
+};
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 d;
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 d;
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ f2 h2f(uint32_t w) {
+    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&w));
+    return f2{v.x, v.y};
+}
+// Codes of eight already-scaled values t = x * inv (binary32, rounded): clamp to
+// +-127 (CLAMP only), round to nearest-even by adding 2^23 + 2^22, and pack the
+// low bytes of the biased floats little-endian into two words.
+template <bool CLAMP>
+__device__ __forceinline__ uint2 pack_codes8(const f2 (&t)[4]) {
+    uint32_t b[8];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        f2 v = t[w];
+        if (CLAMP) {
+            v.x = fminf(fmaxf(v.x, -127.0f), 127.0f);
+            v.y = fminf(fmaxf(v.y, -127.0f), 127.0f);
+        }
+        v = add2(v, f2{12582912.0f, 12582912.0f});
+        b[2 * w] = __float_as_uint(v.x);
+        b[2 * w + 1] = __float_as_uint(v.y);
+    }
+    const uint32_t lo = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    const uint32_t hi = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+    return make_uint2(lo, hi);
+}
+
 constexpr int kQThreads = 256;
 
 // One CTA quantizes one 128-token chunk of one unit: the Q and K rows of the
@@ -308,10 +369,107 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
         bulk_load(smem_u32(sq), static_cast<const T*>(p.q) + ubase + static_cast<size_t>(r0) * D, bytes, smem_u32(&bar));
         bulk_load(smem_u32(sk), static_cast<const T*>(p.k) + ubase + static_cast<size_t>(r0) * D, bytes, smem_u32(&bar));
     }
-    // mean_k (computed by k1_mean_final; zero when smoothing is off).
+    // mean_k (computed by k1_mean_partials; zero when smoothing is off).
     if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
     __syncthreads();
     mbar_wait(smem_u32(&bar), 0);
+
+    if constexpr (std::is_same<T, __half>::value) {
+        // fp16 fast path.  Every thread keeps one 8-channel column block (CV divides
+        // the thread count), so its eight K means live in registers.
+        const int col = (tid % CV) * 8;
+        f2 mc[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) mc[w] = f2{-s_mean[col + 2 * w], -s_mean[col + 2 * w + 1]};
+        // Pass 1.  Q: the group max of |fl(q * fold)| is fl(max|q| * fold) (rounding
+        // is monotone and sign-symmetric), and max|q| is an unsigned 16-bit max over
+        // the fp16 bit patterns with the sign cleared -- which also flags inf / NaN
+        // (>= 0x7C00).  K: the binary32 smooth fl(k - mean) and its group maxima.
+        uint32_t qbits = 0, kbits = 0;
+        float amax_k0 = 0.0f, amax_k1 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int row = (tid + i * kQThreads) / CV;
+            if (row < rows) {
+                const uint4 uq = *reinterpret_cast<const uint4*>(sq + row * D + col);
+                const uint4 uk = *reinterpret_cast<const uint4*>(sk + row * D + col);
+                const uint32_t wq[4] = {uq.x, uq.y, uq.z, uq.w}, wk[4] = {uk.x, uk.y, uk.z, uk.w};
+                float a = 0.0f;
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    qbits = __vmaxu2(qbits, wq[w] & 0x7FFF7FFFu);
+                    kbits = __vmaxu2(kbits, wk[w] & 0x7FFF7FFFu);
+                    const f2 d = add2(h2f(wk[w]), mc[w]);
+                    a = fmaxf(a, fmaxf(fabsf(d.x), fabsf(d.y)));
+                }
+                if (i < VPT / 2) amax_k0 = fmaxf(amax_k0, a);
+                else amax_k1 = fmaxf(amax_k1, a);
+            }
+        }
+        const uint32_t qb = max(qbits & 0xFFFFu, qbits >> 16), kb = max(kbits & 0xFFFFu, kbits >> 16);
+        if (qb >= 0x7C00u || kb >= 0x7C00u) atomicOr(p.status, kStatusNonFinite);
+        const __half qh = __ushort_as_half(static_cast<unsigned short>(qb));
+        float amax_q = __fmul_rn(__half2float(qh), p.fold);
+        amax_q = warp_max(amax_q);
+        amax_k0 = warp_max(amax_k0);
+        amax_k1 = warp_max(amax_k1);
+        if ((tid & 31) == 0) {
+            s_red[tid >> 5][0] = amax_q;
+            s_red[tid >> 5][1] = amax_k0;
+            s_red[tid >> 5][2] = amax_k1;
+        }
+        __syncthreads();
+        if (tid < 3) {
+            float m = 0.0f;
+            for (int w = 0; w < kQThreads / 32; ++w) m = fmaxf(m, s_red[w][tid]);
+            float delta, inv;
+            int8_scale(m, delta, inv);
+            s_inv[tid] = inv;
+            const int ngk = (p.n + kBlockKV - 1) / kBlockKV;
+            if (tid == 0) {
+                p.qscales[static_cast<size_t>(unit) * ((p.n + kBlockQ - 1) / kBlockQ) + chunk] = delta;
+            } else {
+                const int g = 2 * chunk + (tid - 1);
+                if (g < ngk) p.kscales[static_cast<size_t>(unit) * ngk + g] = delta;
+            }
+        }
+        __syncthreads();
+        // Pass 2: codes, recomputing the binary32 fold / smooth from shared memory.
+        const float inv_q = s_inv[0], inv_k0 = s_inv[1], inv_k1 = s_inv[2];
+        const bool clamp = isinf(inv_q) || isinf(inv_k0) || isinf(inv_k1);  // 1/delta overflowed
+        const f2 fold2{p.fold, p.fold}, iq2{inv_q, inv_q};
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const int row = (tid + i * kQThreads) / CV;
+            if (row < rows) {
+                const uint4 uq = *reinterpret_cast<const uint4*>(sq + row * D + col);
+                const uint4 uk = *reinterpret_cast<const uint4*>(sk + row * D + col);
+                const uint32_t wq[4] = {uq.x, uq.y, uq.z, uq.w}, wk[4] = {uk.x, uk.y, uk.z, uk.w};
+                const float ik = i < VPT / 2 ? inv_k0 : inv_k1;
+                const f2 ik2{ik, ik};
+                f2 tq[4], tk[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    tq[w] = mul2(mul2(h2f(wq[w]), fold2), iq2);
+                    tk[w] = mul2(add2(h2f(wk[w]), mc[w]), ik2);
+                }
+                const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
+                *reinterpret_cast<uint2*>(p.qcodes + off) = clamp ? pack_codes8<true>(tq) : pack_codes8<false>(tq);
+                *reinterpret_cast<uint2*>(p.kcodes + off) = clamp ? pack_codes8<true>(tk) : pack_codes8<false>(tk);
+            }
+        }
+        if (p.check_v) {
+            bool vfin = true;
+            for (int v = tid; v < rows * CV; v += kQThreads) {
+                const int row = v / CV, c8 = (v % CV) * 8;
+                float x[8];
+                load8<T>(static_cast<const T*>(p.v) + ubase + static_cast<size_t>(r0 + row) * D + c8, x);
+                vfin &= all_finite8(x);
+            }
+            if (!vfin) atomicOr(p.status, kStatusNonFinite);
+        }
+        return;
+    }
 
     // Pass 1: fold (Q) / smooth (K) in binary32 and the group maxima.
     float amax_q = 0.0f, amax_k0 = 0.0f, amax_k1 = 0.0f, nan_probe = 0.0f;
@@ -418,9 +576,6 @@ cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
             default: return cudaErrorInvalidValue;
         }
         cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        k1_mean_final<D><<<p.units, D, 0, s>>>(p);
-        e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     const dim3 grid((p.n + kBlockQ - 1) / kBlockQ, p.units);

@@ -188,3 +188,16 @@ def test_multi_shard_host_path_equals_single(cuda):
     o1 = attention_fwd_host(q, k, v, True, np.empty(q.shape, np.float32), devices=[0])
     o2 = attention_fwd_host(q, k, v, True, np.empty(q.shape, np.float32), devices=[0, 0, 0, 0])
     assert np.array_equal(o1, o2)
+
+
+def test_host_path_many_chunks_equals_device_path(cuda):
+    """Host path with many unit chunks (per-chunk K1 counters and status words) equals the device call."""
+    import torch
+
+    from paper_2410_02367_b200 import attention_fwd_host, sage_attention_cuda
+
+    q, k, v = (x.astype(np.float16) for x in _qkv(2, 40, 200, 64))
+    oh = attention_fwd_host(q, k, v, False, np.empty(q.shape, np.float32), devices=[0])
+    qd, kd, vd = (torch.from_numpy(x).cuda() for x in (q, k, v))
+    od = sage_attention_cuda(qd, kd, vd, causal=False, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(oh, od)
