@@ -40,6 +40,7 @@
 // exact in real arithmetic because l and O share the stale max.
 #include <cuda.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "sab_internal.h"
@@ -596,10 +597,16 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
         !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, kBN, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     // Raster groups: as few groups as keep each group's K^ (int8) and V (fp16) within
-    // ~96 MB of the 126 MB L2, balanced in size.
+    // ~32 MB of the 126 MB L2, balanced in size (24-48 MB measured best on C2 and C4;
+    // scripts/l2sweep.sh).
     AttnParams pp = p;
     const size_t kv_unit = static_cast<size_t>(p.n) * D * 3;
-    const size_t per_group = std::max<size_t>(1, (96u << 20) / kv_unit);
+    static const size_t budget = [] {  // SAB_L2_GROUP_MB overrides the default (tuning)
+        const char* e = std::getenv("SAB_L2_GROUP_MB");
+        const long mb = e ? std::atol(e) : 32;
+        return static_cast<size_t>(mb > 0 ? mb : 32) << 20;
+    }();
+    const size_t per_group = std::max<size_t>(1, budget / kv_unit);
     const size_t groups = (static_cast<size_t>(p.units) + per_group - 1) / per_group;
     pp.group_units = static_cast<int>((static_cast<size_t>(p.units) + groups - 1) / groups);
     auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP>;
