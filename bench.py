@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C2")
+    ap.add_argument("--variant", default="B", choices=["B", "T"],
+                    help="B: SAGEAttn-B (per-block Q/K scales, the north-star path); T: SAGEAttn-T (per-token)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -214,7 +216,8 @@ def main():
     units_total = batch * wl["heads"]
     n, d, causal = wl["tokens"], wl["head_dim"], wl["causal"]
     total_ops = paper_ops(units_total, n, d, causal)
-    config = {"workload": wl["name"], "batch": batch, "heads": wl["heads"], "tokens": n, "head_dim": d,
+    per_token = args.variant == "T"
+    config = {"workload": wl["name"], "variant": f"SAGEAttn-{args.variant}", "batch": batch, "heads": wl["heads"], "tokens": n, "head_dim": d,
               "causal": causal, "global_batch": batch,
               "parallelism": (f"head x batch shard over {world} GPUs, no collective" if world > 1 else "single GPU"),
               "scaling_mode": args.scaling + (" (batch grows with GPUs; units per GPU fixed)" if args.scaling == "weak"
@@ -277,7 +280,7 @@ def main():
         data = "synthetic N(0,1) fp16 (torch.randn, seeded per shard)"
     q, k, v = (h.to(dev) for h in host)
     o = torch.empty_like(q)
-    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16)
+    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16, per_token=per_token)
     ws = sageattn.Workspace(desc, dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -324,12 +327,12 @@ def main():
         e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
         hq, hk, hv = (h.contiguous().pin_memory().numpy() for h in host)
         ho = torch.empty(hq.shape, dtype=torch.float16).pin_memory().numpy()
-        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index])  # warm the context pool
+        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token)  # warm pool
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index])
+            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token)
         e2e_s = time.perf_counter() - t0
 
     local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s], dtype=torch.float64, device=red_dev)
@@ -363,7 +366,8 @@ def main():
     if rank != 0:
         return
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": METRIC if not per_token else METRIC.replace("SageAttn-B", "SageAttn-T"), "value": value,
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int8 QK^T (s32 acc) / fp16 PV (fp32 acc); fp16 Q/K/V/O",
         "data": data, "config": config,
@@ -382,7 +386,7 @@ def main():
                         "ms_per_step": k1_mean_ms, "alg_bytes": k1_alg, "min_dram_bytes_with_k_reread": k1_bytes},
         "clocks": sampler.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not per_token:
         threads = args.cpu_threads or os.cpu_count() or 1
         v_cpu, s_cpu, sdesc, used, kind = cpu_reference_sample(wl, threads)
         line["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": used, "kind": kind, "sample": sdesc,

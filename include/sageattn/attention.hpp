@@ -1,9 +1,9 @@
-// sageattn/attention.hpp -- B200 drop-in for the reference's SAGEAttn-B entry point.
+// sageattn/attention.hpp -- B200 drop-in for the reference's SAGEAttn-B / -T entry point.
 //
 // Source-compatible replacement for /root/reference/proj/include/sageattn/
 // attention.hpp as far as the SAGEAttn-B hot path goes: an application that
 // calls
-//     sageattn::sage_attention(const AttentionInput&, SageVariant::B, const SageOptions&)
+//     sageattn::sage_attention(const AttentionInput&, SageVariant::B | SageVariant::T, const SageOptions&)
 //     sageattn::sage_attention(const AttentionInput&, const KernelConfig&, const SageOptions&)
 // (attention.hpp:318-319, 547-550) switches to the B200 path by putting
 // <repo>/include first on its include path and linking
@@ -21,9 +21,9 @@
 //     P~V accumulator (attention.hpp:84-102, 321, 531-533);
 //   * pure / re-entrant calls (per-call device contexts, attention.hpp:9-12).
 // Differences (documented in INTEGRATION.md):
-//   * only SAGEAttn-B (PerBlock Q/K, Fp16Acc P~V, block 128/64, INT8) runs; other
-//     variants, FP8 dtypes or block sizes throw std::invalid_argument -- there is
-//     no CPU fallback;
+//   * only SAGEAttn-B (PerBlock Q/K) and SAGEAttn-T (PerToken Q/K) with Fp16Acc P~V,
+//     block 128/64 and INT8 run; vB/vT, FP8 dtypes or other block sizes throw
+//     std::invalid_argument -- there is no CPU fallback;
 //   * head_dim must be 64 or 128;
 //   * P~V accumulates in FP32 on the tensor cores (the reference's
 //     pv_fp32_accumulator arm) whatever pv_fp32_accumulator says; Q^/K^ codes,
@@ -165,8 +165,10 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
         throw std::invalid_argument("sage_attention: block sizes must be >= 1");
     if (!in.q.same_shape(in.k) || !in.q.same_shape(in.v))
         throw std::invalid_argument("sage_attention: Q, K, V shapes differ");
-    if (config.qk_granularity != QkGranularity::PerBlock || config.pv_path != PvPath::Fp16Acc)
-        throw std::invalid_argument("sage_attention: only SAGEAttn-B (PerBlock Q/K, FP16 P~V) runs on the B200 path");
+    if ((config.qk_granularity != QkGranularity::PerBlock && config.qk_granularity != QkGranularity::PerToken) ||
+        config.pv_path != PvPath::Fp16Acc)
+        throw std::invalid_argument(
+            "sage_attention: only SAGEAttn-B / SAGEAttn-T (PerBlock or PerToken Q/K, FP16 P~V) run on the B200 path");
     if (options.qk_dtype != QuantDtype::Int8)
         throw std::invalid_argument("sage_attention: only INT8 Q/K quantization runs on the B200 path");
 
@@ -178,6 +180,7 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
     d.block_kv = config.block_kv;
     d.smooth_k = options.smooth_k ? 1 : 0;
     d.check_v = 1;  // validate_input scans V too (attention.hpp:101)
+    d.qk_granularity = config.qk_granularity == QkGranularity::PerToken ? SAB_QK_PER_TOKEN : SAB_QK_PER_BLOCK;
     Tensor4f out(in.q.batch, in.q.heads, in.q.tokens, in.q.head_dim);
     int n_dev = b200::device_count_override();
     if (n_dev <= 0) sab_device_count(&n_dev);

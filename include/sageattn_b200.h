@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define SAB_ABI_VERSION 1
+#define SAB_ABI_VERSION 2
 
 /* Status codes.  The C++ shim maps them back to the reference's exceptions:
  * SAB_ERR_SHAPE / SAB_ERR_NONFINITE / SAB_ERR_UNSUPPORTED -> std::invalid_argument,
@@ -52,8 +52,13 @@ enum sab_dtype { SAB_F16 = 0, SAB_F32 = 1 };
  * FP32 output. */
 enum sab_pv_accum { SAB_PV_FP32 = 0, SAB_PV_FP16_TILE = 1 };
 
+/* Q/K scale granularity: KernelConfig::qk_granularity (attention.hpp:34, 41-46).
+ * PER_BLOCK = SAGEAttn-B (128-token Q groups, 64-token K groups); PER_TOKEN =
+ * SAGEAttn-T (one scale per token; kernel_config_for(T), attention.hpp:50). */
+enum sab_qk_granularity { SAB_QK_PER_BLOCK = 0, SAB_QK_PER_TOKEN = 1 };
+
 /* Call descriptor: the shape of AttentionInput (attention.hpp:27-32) plus the
- * KernelConfig/SageOptions fields the B path reads (attention.hpp:41-46, 71-77). */
+ * KernelConfig/SageOptions fields the B/T paths read (attention.hpp:41-46, 71-77). */
 typedef struct sab_desc {
     int32_t batch, heads, tokens, head_dim;
     int32_t causal;       /* AttentionInput::causal                                */
@@ -64,6 +69,7 @@ typedef struct sab_desc {
     int32_t smooth_k;     /* SageOptions::smooth_k                                 */
     int32_t pv_accum;     /* sab_pv_accum                                          */
     int32_t check_v;      /* 1: scan V for non-finite values (validate_input)      */
+    int32_t qk_granularity; /* sab_qk_granularity (ABI 2)                            */
 } sab_desc;
 
 /* Fills *d with the SAGEAttn-B defaults (kernel_config_for(B), attention.hpp:51;
@@ -74,8 +80,8 @@ void sab_desc_init(sab_desc* d, int32_t batch, int32_t heads, int32_t tokens, in
 typedef struct sab_ws_layout {
     uint64_t qcodes;    /* int8  [units][tokens][head_dim]  Q^ (quant.hpp:128-173)   */
     uint64_t kcodes;    /* int8  [units][tokens][head_dim]  K^                        */
-    uint64_t qscales;   /* float [units][ceil(tokens/128)]  delta_Q                    */
-    uint64_t kscales;   /* float [units][ceil(tokens/64)]   delta_K                    */
+    uint64_t qscales;   /* float [units][ceil(tokens/128)]  delta_Q  (per token: [units][npad],    */
+    uint64_t kscales;   /* float [units][ceil(tokens/64)]   delta_K   npad = 64*ceil(tokens/64))   */
     uint64_t mean_k;    /* float [units][head_dim]          SmoothState::mean_k        */
     uint64_t partials;  /* float [units][n_partials][head_dim] mean tree partial sums  */
     uint64_t v16;       /* fp16  [units][tokens][head_dim]  V on the fp16 grid (F32 in)*/

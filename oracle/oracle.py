@@ -73,6 +73,8 @@ class Oracle:
                                          C.c_int, C.c_int, C.c_int, C.c_int, _f32p, _u64p]
         lib.orc_sage_b.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_int, _f32p, _u64p]
+        lib.orc_sage.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 8 + [_f32p, _u64p]
+        lib.orc_sage_tiles.argtypes = [_i8p, _f32p, _i8p, _f32p, _f32p] + [C.c_int] * 10 + [_f32p, _u64p]
         lib.orc_naive.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
         self.lib = lib
 
@@ -84,11 +86,14 @@ class Oracle:
         return self.lib.orc_half_bits(float(x))
 
     # -- prepass ----------------------------------------------------------
-    def prepass(self, q, k, smooth=True, block_q=BLOCK_Q, block_kv=BLOCK_KV):
-        """Per-unit fold+quantize(Q) and smooth+quantize(K).
+    def prepass(self, q, k, smooth=True, block_q=BLOCK_Q, block_kv=BLOCK_KV, per_token=False):
+        """Per-unit fold+quantize(Q) and smooth+quantize(K); per_token: one scale per
+        token (variant T, Granularity::per_token = groups of one row).
 
         Returns dict(qcodes, qscales, kcodes, kscales, mean) or raises
         ValueError on non-finite input."""
+        if per_token:
+            block_q = block_kv = 1
         q, k = _f32(q), _f32(k)
         units, n, d = q.shape
         gq, gk = -(-n // block_q), -(-n // block_kv)
@@ -143,6 +148,38 @@ class Oracle:
             raise RuntimeError(f"oracle failed: {st}")
         return out, macs
 
+    def sage(self, q, k, v, causal=False, smooth=True, pv_fp32=True, per_token=False, threads=None):
+        """SAGEAttn-B (per_token=False) or SAGEAttn-T (per_token=True) forward; returns (out, macs)."""
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        units, n, d = q.shape
+        out = np.empty_like(q)
+        macs = np.zeros(2, np.uint64)
+        st = self.lib.orc_sage(q, k, v, units, n, d, int(causal), int(smooth), int(pv_fp32), int(per_token),
+                               threads or os.cpu_count() or 1, out, macs)
+        if st == 2:
+            raise ValueError("sage_attention: non-finite input")
+        if st == 3:
+            raise OverflowError("sage_attention: binary16 P~V accumulator overflowed")
+        if st != 0:
+            raise RuntimeError(f"oracle failed: {st}")
+        return out, macs
+
+    def sage_tiles(self, pre, v, unit, tiles, causal, pv_fp32=True, per_token=False):
+        """sage_b_tiles for either variant (per_token: scale groups of one token)."""
+        v = _f32(v)
+        n, d = v.shape[1:]
+        g_q, g_k = (1, 1) if per_token else (BLOCK_Q, BLOCK_KV)
+        out = np.zeros((n, d), np.float32)
+        macs = np.zeros(2, np.uint64)
+        for t in tiles:
+            st = self.lib.orc_sage_tiles(np.ascontiguousarray(pre["qcodes"][unit]), np.ascontiguousarray(pre["qscales"][unit]),
+                                         np.ascontiguousarray(pre["kcodes"][unit]), np.ascontiguousarray(pre["kscales"][unit]),
+                                         np.ascontiguousarray(v[unit]), n, d, int(causal), int(pv_fp32), BLOCK_Q, BLOCK_KV,
+                                         g_q, g_k, int(t), int(t) + 1, out, macs)
+            if st != 0:
+                raise RuntimeError(f"oracle tiles failed: {st}")
+        return out
+
     def sage_b_tiles(self, pre, v, unit, tiles, causal, pv_fp32=True):
         """Query tiles `tiles` of one unit from prepass outputs `pre`; returns (N,d) with only those rows set."""
         v = _f32(v)
@@ -192,6 +229,8 @@ class Reference:
         lib.ref_naive_attention.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 5 + [_f64p]
         lib.ref_sage_b_tiles.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, _intp, C.c_int,
                                          _f32p]
+        lib.ref_quantize_qk_per_token.argtypes = [_f32p, _f32p] + [C.c_int] * 5 + [_i8p, _f32p, _i8p, _f32p]
+        lib.ref_sage_attention_variant.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 8 + [_f32p]
         self.lib = lib
 
     def _raise(self, st):
@@ -237,6 +276,28 @@ class Reference:
         if st:
             self._raise(st)
         return codes, scales
+
+    def quantize_per_token(self, q4, k4, smooth=True):
+        """Variant T prepass: (qcodes, qscales[units][N], kcodes, kscales[units][N])."""
+        q4, k4 = _f32(q4), _f32(k4)
+        b, h, n, d = q4.shape
+        qc, kc = np.empty(q4.shape, np.int8), np.empty(k4.shape, np.int8)
+        qs, ks = np.empty((b * h, n), np.float32), np.empty((b * h, n), np.float32)
+        st = self.lib.ref_quantize_qk_per_token(q4, k4, b, h, n, d, int(smooth), qc, qs, kc, ks)
+        if st:
+            self._raise(st)
+        return qc, qs, kc, ks
+
+    def sage_attention_variant(self, q4, k4, v4, variant="T", causal=False, smooth=True, pv_fp32=False):
+        """sageattn::sage_attention(in, SageVariant::T|B, opts)."""
+        q4, k4, v4 = _f32(q4), _f32(k4), _f32(v4)
+        b, h, n, d = q4.shape
+        out = np.empty_like(q4)
+        st = self.lib.ref_sage_attention_variant(q4, k4, v4, b, h, n, d, int(causal), 0 if variant == "T" else 1,
+                                                 int(smooth), int(pv_fp32), out)
+        if st:
+            self._raise(st)
+        return out
 
     def int8_tile(self, qc, kc, r0, bq, c0, bkv):
         n, d = qc.shape

@@ -89,6 +89,42 @@ int ref_quantize_k(const float* k, int b, int h, int n, int d, int block_kv, int
     } catch (const std::invalid_argument& e) { return fail(e, 1); }
 }
 
+// The T-path prepass (kernel_config_for(T), attention.hpp:50): Granularity::per_token()
+// for both psi_Q (folded Q) and psi_K (smoothed K) (attention.hpp:255-262, 344-359).
+int ref_quantize_qk_per_token(const float* q, const float* k, int b, int h, int n, int d, int smooth, int8_t* qcodes,
+                              float* qscales, int8_t* kcodes, float* kscales) {
+    try {
+        const Tensor4f qf = fold_scale_into_q(make4(q, b, h, n, d), d);
+        Tensor4f ks = make4(k, b, h, n, d);
+        if (smooth) ks = smooth_k(ks).first;
+        for (int u = 0; u < b * h; ++u) {
+            QuantizedMatrix qm = quantize(qf.slice(u / h, u % h), Granularity::per_token(), QuantDtype::Int8);
+            QuantizedMatrix km = quantize(ks.slice(u / h, u % h), Granularity::per_token(), QuantDtype::Int8);
+            std::memcpy(qcodes + size_t(u) * n * d, qm.codes.data(), qm.codes.size());
+            std::memcpy(qscales + size_t(u) * n, qm.scales.data(), sizeof(float) * n);
+            std::memcpy(kcodes + size_t(u) * n * d, km.codes.data(), km.codes.size());
+            std::memcpy(kscales + size_t(u) * n, km.scales.data(), sizeof(float) * n);
+        }
+        return 0;
+    } catch (const std::invalid_argument& e) { return fail(e, 1); }
+}
+
+// sage_attention(in, SageVariant v, opts) (attention.hpp:547-550) for v = 0 (T) or 1 (B).
+int ref_sage_attention_variant(const float* q, const float* k, const float* v, int b, int h, int n, int d, int causal,
+                               int variant, int smooth, int pv_fp32, float* out) {
+    try {
+        AttentionInput in{make4(q, b, h, n, d), make4(k, b, h, n, d), make4(v, b, h, n, d), causal != 0};
+        SageOptions opt;
+        opt.smooth_k = smooth != 0;
+        opt.pv_fp32_accumulator = pv_fp32 != 0;
+        Tensor4f o = sage_attention(in, variant == 0 ? SageVariant::T : SageVariant::B, opt);
+        std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+        return 0;
+    } catch (const std::invalid_argument& e) { return fail(e, 1); } catch (const std::overflow_error& e) {
+        return fail(e, 3);
+    }
+}
+
 // detail::int8_tile_nt (attention.hpp:265-279) on raw code matrices.
 int ref_int8_tile(const int8_t* qc, const int8_t* kc, int n, int d, int r0, int bq, int c0, int bkv, int32_t* out) {
     QuantizedMatrix qm, km;

@@ -238,9 +238,9 @@ int orc_causal_tile(int i, int j, int block_q, int block_kv, int n)
  * Returns ORC_ERR_OVERFLOW when the binary16 accumulator overflowed
  * (attention.hpp:531-533).  macs[0..1] accumulate the SageDiagnostics MAC
  * counters (attention.hpp:404, 445) when non-NULL. */
-int orc_sage_b_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const float* ks, const float* v, int n,
-                     int d, int causal, int pv_fp32, int block_q, int block_kv, int qt0, int qt1, float* out,
-                     uint64_t* macs)
+int orc_sage_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const float* ks, const float* v, int n, int d,
+                   int causal, int pv_fp32, int block_q, int block_kv, int gq, int gk, int qt0, int qt1, float* out,
+                   uint64_t* macs)
 {
     const int n_kv = (n + block_kv - 1) / block_kv;
     int32_t* acc = (int32_t*)malloc(sizeof(int32_t) * (size_t)block_q * block_kv);
@@ -260,7 +260,6 @@ int orc_sage_b_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const 
     for (int i = qt0; i < qt1; ++i) {
         const int r0 = i * block_q;
         const int bq = (block_q < n - r0) ? block_q : n - r0;
-        const float dq = qs[i];
         for (int r = 0; r < bq; ++r) {
             m[r] = -INFINITY;
             l[r] = 0.0f;
@@ -276,10 +275,14 @@ int orc_sage_b_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const 
             }
             if (macs) macs[0] += (uint64_t)bq * bkv * d;
             orc_int8_tile_nt(qc, kc, d, r0, bq, c0, bkv, acc, block_kv);
-            /* s = (float(acc) * dq) * dk  (attention.hpp:409-414). */
-            for (int r = 0; r < bq; ++r)
+            /* s = (float(acc) * dq) * dk  (attention.hpp:409-414); scale groups of gq / gk
+             * tokens (Granularity::group_of, quant.hpp:56-63: per_block(b) -> r / b,
+             * per_token -> r). */
+            for (int r = 0; r < bq; ++r) {
+                const float dq = qs[(r0 + r) / gq];
                 for (int c = 0; c < bkv; ++c)
-                    s[r * block_kv + c] = ((float)acc[r * block_kv + c] * dq) * ks[(c0 + c) / block_kv];
+                    s[r * block_kv + c] = ((float)acc[r * block_kv + c] * dq) * ks[(c0 + c) / gk];
+            }
             if (kind == 1)
                 for (int r = 0; r < bq; ++r)
                     for (int c = 0; c < bkv; ++c)
@@ -340,27 +343,44 @@ done:
     return status;
 }
 
-/* Whole SAGEAttn-B forward for one unit (attention.hpp:318-545, variant B
- * = PerBlock(128/64) + Fp16Acc). */
-int orc_sage_b_unit(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth,
-                    int pv_fp32, float* out, uint64_t* macs)
+/* The variant B tile loop: scale groups equal to the tiles (per_block(128 / 64)). */
+int orc_sage_b_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const float* ks, const float* v, int n,
+                     int d, int causal, int pv_fp32, int block_q, int block_kv, int qt0, int qt1, float* out,
+                     uint64_t* macs)
+{
+    return orc_sage_tiles(qc, qs, kc, ks, v, n, d, causal, pv_fp32, block_q, block_kv, block_q, block_kv, qt0, qt1,
+                          out, macs);
+}
+
+/* Whole SAGEAttn forward for one unit (attention.hpp:318-545): variant B =
+ * PerBlock(128/64) + Fp16Acc, variant T (per_token) = PerToken + Fp16Acc with the
+ * same 128 x 64 tiles (kernel_config_for, attention.hpp:48-55). */
+int orc_sage_unit(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth, int pv_fp32,
+                  int per_token, float* out, uint64_t* macs)
 {
     const int bq = 128, bkv = 64;
+    const int gq = per_token ? 1 : bq, gk = per_token ? 1 : bkv;
     for (size_t i = 0; i < (size_t)n * d; ++i)
         if (!isfinite(v[i])) return ORC_ERR_NONFINITE;
     int8_t* qc = (int8_t*)malloc((size_t)n * d);
     int8_t* kc = (int8_t*)malloc((size_t)n * d);
-    float* qs = (float*)malloc(sizeof(float) * (size_t)((n + bq - 1) / bq));
-    float* ks = (float*)malloc(sizeof(float) * (size_t)((n + bkv - 1) / bkv));
+    float* qs = (float*)malloc(sizeof(float) * (size_t)((n + gq - 1) / gq));
+    float* ks = (float*)malloc(sizeof(float) * (size_t)((n + gk - 1) / gk));
     int st = ORC_ERR_NOMEM;
     if (qc && kc && qs && ks) {
-        st = orc_prepass_unit(q, k, n, d, bq, bkv, smooth, qc, qs, kc, ks, NULL);
+        st = orc_prepass_unit(q, k, n, d, gq, gk, smooth, qc, qs, kc, ks, NULL);
         if (st == ORC_OK)
-            st = orc_sage_b_tiles(qc, qs, kc, ks, v, n, d, causal, pv_fp32, bq, bkv, 0, (n + bq - 1) / bq, out,
-                                  macs);
+            st = orc_sage_tiles(qc, qs, kc, ks, v, n, d, causal, pv_fp32, bq, bkv, gq, gk, 0, (n + bq - 1) / bq,
+                                out, macs);
     }
     free(qc); free(kc); free(qs); free(ks);
     return st;
+}
+
+int orc_sage_b_unit(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth,
+                    int pv_fp32, float* out, uint64_t* macs)
+{
+    return orc_sage_unit(q, k, v, n, d, causal, smooth, pv_fp32, 0, out, macs);
 }
 
 /* Exact binary64 attention for one unit (attention.hpp:110-149). */
@@ -396,7 +416,7 @@ typedef struct {
     const float *q, *k, *v;
     float* out;
     double* out64;
-    int units, n, d, causal, smooth, pv_fp32, naive;
+    int units, n, d, causal, smooth, pv_fp32, naive, per_token;
     int next;
     int status;
     uint64_t macs[2];
@@ -417,8 +437,8 @@ static void* orc_worker(void* arg)
         if (job->naive)
             orc_naive_unit(job->q + off, job->k + off, job->v + off, job->n, job->d, job->causal, job->out64 + off);
         else
-            st = orc_sage_b_unit(job->q + off, job->k + off, job->v + off, job->n, job->d, job->causal, job->smooth,
-                                 job->pv_fp32, job->out + off, macs);
+            st = orc_sage_unit(job->q + off, job->k + off, job->v + off, job->n, job->d, job->causal, job->smooth,
+                               job->pv_fp32, job->per_token, job->out + off, macs);
         if (st != ORC_OK) {
             pthread_mutex_lock(&job->mu);
             if (job->status == ORC_OK) job->status = st;
@@ -446,15 +466,22 @@ static int orc_run(orc_job* job, int threads, uint64_t* macs)
     return job->status;
 }
 
-int orc_sage_b(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,
-               int pv_fp32, int threads, float* out, uint64_t* macs)
+int orc_sage(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,
+             int pv_fp32, int per_token, int threads, float* out, uint64_t* macs)
 {
     if (units < 1 || n < 1 || d < 1) return ORC_ERR_SHAPE;
     orc_job job;
     memset(&job, 0, sizeof(job));
     job.q = q; job.k = k; job.v = v; job.out = out;
     job.units = units; job.n = n; job.d = d; job.causal = causal; job.smooth = smooth; job.pv_fp32 = pv_fp32;
+    job.per_token = per_token;
     return orc_run(&job, threads, macs);
+}
+
+int orc_sage_b(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,
+               int pv_fp32, int threads, float* out, uint64_t* macs)
+{
+    return orc_sage(q, k, v, units, n, d, causal, smooth, pv_fp32, 0, threads, out, macs);
 }
 
 int orc_naive(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int threads,

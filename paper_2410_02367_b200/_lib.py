@@ -25,6 +25,8 @@ SAB_F16 = 0
 SAB_F32 = 1
 SAB_PV_FP32 = 0
 SAB_PV_FP16_TILE = 1
+SAB_QK_PER_BLOCK = 0  # SAGEAttn-B
+SAB_QK_PER_TOKEN = 1  # SAGEAttn-T
 
 # Every symbol include/sageattn_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
@@ -38,7 +40,7 @@ EXPORTS = (
 class SabDesc(C.Structure):
     _fields_ = [(name, C.c_int32) for name in (
         "batch", "heads", "tokens", "head_dim", "causal", "in_dtype", "out_dtype", "block_q", "block_kv",
-        "smooth_k", "pv_accum", "check_v")]
+        "smooth_k", "pv_accum", "check_v", "qk_granularity")]
 
 
 class SabWsLayout(C.Structure):
@@ -102,12 +104,13 @@ def check(status: int):
 
 
 def desc(batch, heads, tokens, head_dim, causal=False, in_dtype=SAB_F16, out_dtype=SAB_F32, block_q=128,
-         block_kv=64, smooth_k=True, pv_accum=SAB_PV_FP32, check_v=False) -> SabDesc:
+         block_kv=64, smooth_k=True, pv_accum=SAB_PV_FP32, check_v=False, per_token=False) -> SabDesc:
     d = SabDesc()
     load().sab_desc_init(C.byref(d), batch, heads, tokens, head_dim, int(causal))
     d.in_dtype, d.out_dtype = in_dtype, out_dtype
     d.block_q, d.block_kv = block_q, block_kv
     d.smooth_k, d.pv_accum, d.check_v = int(smooth_k), pv_accum, int(check_v)
+    d.qk_granularity = SAB_QK_PER_TOKEN if per_token else SAB_QK_PER_BLOCK
     return d
 
 

@@ -253,7 +253,81 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
     return alpha;
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP>
+// SAGEAttn-T variant of softmax_half: per-token scales, so the dequant factor
+// w = dQ[row] * dK[key] * log2 e differs per element and the row max is taken on
+// the scaled scores (attention.hpp:409-414 with per_token group_of, quant.hpp:56-63).
+// dkp points at this thread's 32 key scales (K1 pads each unit's scale row to a
+// multiple of 64, so the float4 loads stay in bounds); r is overwritten with the
+// scores.  Same contract as softmax_half otherwise.
+template <bool MASK, bool CAUSAL>
+__device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts, int half, float dq, const float* dkp,
+                                                 int kb, int qi, int n, float& m, float& l, bool& rescale,
+                                                 int32_t* dump) {
+    const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
+    if (dump) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 4)  // the raw INT32 accumulators (bias removed)
+            *reinterpret_cast<int4*>(dump + c) = make_int4(r[c] - kMagicI, r[c + 1] - kMagicI, r[c + 2] - kMagicI,
+                                                           r[c + 3] - kMagicI);
+    }
+    const int lim2 = MASK ? opaque(lim) : lim;
+    float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const float4 dk4 = __ldg(reinterpret_cast<const float4*>(dkp) + g);
+        const f2 w0 = ffma2(f2{dq, dq}, f2{dk4.x, dk4.y}, f2{0.0f, 0.0f});
+        const f2 w1 = ffma2(f2{dq, dq}, f2{dk4.z, dk4.w}, f2{0.0f, 0.0f});
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+            const int c = 4 * g + e;
+            // float(acc) exactly: the biased bits minus 2^23 + 2^22.
+            const f2 a = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-kMagicF, -kMagicF});
+            f2 sv = ffma2(a, e == 0 ? w0 : w1, f2{0.0f, 0.0f});
+            if (MASK) {
+                sv.x = (c >= lim2) ? -INFINITY : sv.x;
+                sv.y = (c + 1 >= lim2) ? -INFINITY : sv.y;
+            }
+            mx4[g & 3] = fmaxf(mx4[g & 3], fmaxf(sv.x, sv.y));
+            r[c] = __float_as_uint(sv.x);
+            r[c + 1] = __float_as_uint(sv.y);
+        }
+    }
+    float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    const float m_new = fmaxf(m, mx);
+    rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
+    float alpha = 1.0f;
+    if (rescale) {
+        alpha = ex2(m - m_new);
+        m = m_new;
+    }
+    const float mref = (m == -INFINITY) ? 0.0f : m;
+    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int c = 2 * i;
+        const f2 t = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-mref, -mref});
+        f2 pp;
+        if ((c & 15) >= 16 - kPolyPer16) {
+            pp = exp2_poly2(t);
+        } else {
+            pp = f2{ex2(t.x), ex2(t.y)};
+        }
+        if (MASK) {
+            pp.x = (c >= lim2) ? 0.0f : pp.x;
+            pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+        }
+        pk[i] = pack_half2(pp.x, pp.y);
+        acc[i & 3] = fadd2(acc[i & 3], pp);
+    }
+    tmem_st16x2_16(ts, pk);
+    const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+    l = fmaf(l, alpha, sum.x + sum.y);
+    return alpha;
+}
+
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -446,10 +520,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qi = qt * kBM + row;
         float m = -INFINITY, l = 0.0f;
         if (nkv_x > 0) {
-            const float qsl = p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
-            const float* ksc = p.kscales + static_cast<size_t>(unit) * ntk;
+            // Scale rows: per block [units][ntq] / [units][ntk]; per token (T) [units][npad],
+            // npad = ntk * 64 (K1 pads each unit's rows so 64-key tiles stay in bounds).
+            const int npad = ntk * kBN;
+            const float qsl = PT ? (qi < n ? p.qscales[static_cast<size_t>(unit) * npad + qi] : 1.0f) * kLog2e
+                                 : p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
+            const float* ksc = p.kscales + static_cast<size_t>(unit) * (PT ? npad : ntk);
             // The K scale of the next KV tile is fetched one iteration ahead.
-            float ks_next = __ldg(ksc);
+            float ks_next = PT ? 0.0f : __ldg(ksc);
             const bool tr = (warp % 8) == 0 && lane == 0;
             // Software pipeline: S(j+1) is loaded from TMEM while P(j) is stored and
             // handed to the MMA issuer, so the load latency is off the per-tile chain.
@@ -460,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld16x2_32(tbase + lane_off + x * 128, r);
             for (int j = 0; j < nkv_x; ++j) {
                 const float ks_cur = ks_next;
-                if (j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
+                if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
                 const int b = j & 1;
                 tmem_wait_ld_dep(r);
                 if (tr) SAB_STAMP(x, j, 1);
@@ -474,10 +552,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
                 bool rescale;
                 float alpha;
-                if (need_mask)
+                if (PT) {
+                    const float* dkp = ksc + kb + 32 * half;
+                    if (need_mask)
+                        alpha = softmax_half_pt<true, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
+                    else
+                        alpha = softmax_half_pt<false, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
+                } else if (need_mask) {
                     alpha = softmax_half<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
-                else
+                } else {
                     alpha = softmax_half<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
+                }
                 if (tr) SAB_STAMP(x, j, 2);
                 if (rescale && j > 0) {
                     // O_x must hold P(j-1)V(j-1) before it is rescaled.  PV_x(j-2) is complete
@@ -587,7 +672,7 @@ bool make_map(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int ele
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP>
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT>
 cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     using C = Cfg<D>;
     CUtensorMap tq, tk, tv;
@@ -609,7 +694,7 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     const size_t per_group = std::max<size_t>(1, budget / kv_unit);
     const size_t groups = (static_cast<size_t>(p.units) + per_group - 1) / per_group;
     pp.group_units = static_cast<int>((static_cast<size_t>(p.units) + groups - 1) / groups);
-    auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP>;
+    auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP, PT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int ntq = (p.n + kBM - 1) / kBM;
@@ -622,18 +707,25 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <bool DUMP>
-cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
+template <bool DUMP, bool PT>
+cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
     const bool c = p.causal != 0, f = p.out_f32 != 0;
     if (p.d == 128) {
-        if (c) return f ? launch_k2<128, true, true, DUMP>(p, s) : launch_k2<128, true, false, DUMP>(p, s);
-        return f ? launch_k2<128, false, true, DUMP>(p, s) : launch_k2<128, false, false, DUMP>(p, s);
+        if (c) return f ? launch_k2<128, true, true, DUMP, PT>(p, s) : launch_k2<128, true, false, DUMP, PT>(p, s);
+        return f ? launch_k2<128, false, true, DUMP, PT>(p, s) : launch_k2<128, false, false, DUMP, PT>(p, s);
     }
     if (p.d == 64) {
-        if (c) return f ? launch_k2<64, true, true, DUMP>(p, s) : launch_k2<64, true, false, DUMP>(p, s);
-        return f ? launch_k2<64, false, true, DUMP>(p, s) : launch_k2<64, false, false, DUMP>(p, s);
+        if (c) return f ? launch_k2<64, true, true, DUMP, PT>(p, s) : launch_k2<64, true, false, DUMP, PT>(p, s);
+        return f ? launch_k2<64, false, true, DUMP, PT>(p, s) : launch_k2<64, false, false, DUMP, PT>(p, s);
     }
     return cudaErrorInvalidValue;
+}
+
+// The INT32 S dump does not read the scales, so it only needs the per-block build.
+template <bool DUMP>
+cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
+    if (!DUMP && p.per_token) return dispatch_pt<false, true>(p, s);
+    return dispatch_pt<DUMP, false>(p, s);
 }
 
 }  // namespace

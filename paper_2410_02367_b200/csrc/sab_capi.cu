@@ -53,8 +53,10 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     };
     L->qcodes = take(units * n * hd);
     L->kcodes = take(units * n * hd);
-    L->qscales = take(units * ((n + kBlockQ - 1) / kBlockQ) * sizeof(float));
-    L->kscales = take(units * ((n + kBlockKV - 1) / kBlockKV) * sizeof(float));
+    const bool pt = d->qk_granularity == SAB_QK_PER_TOKEN;
+    const size_t npad = (n + kBlockKV - 1) / kBlockKV * kBlockKV;  // per-token rows padded to 64 tokens
+    L->qscales = take(units * (pt ? npad : (n + kBlockQ - 1) / kBlockQ) * sizeof(float));
+    L->kscales = take(units * (pt ? npad : (n + kBlockKV - 1) / kBlockKV) * sizeof(float));
     L->mean_k = take(units * hd * sizeof(float));
     L->partials = take(units * size_t(n_partials) * hd * sizeof(float));
     L->v16 = take(d->in_dtype == SAB_F32 ? units * n * hd * 2 : 0);
@@ -92,6 +94,7 @@ PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const vo
     p.nodes_per_cta = nodes_per_cta(L.tree_depth);
     p.n_partials = L.n_partials;
     p.smooth = d->smooth_k != 0;
+    p.per_token = d->qk_granularity == SAB_QK_PER_TOKEN;
     p.check_v = d->check_v != 0;
     p.in_f32 = d->in_dtype == SAB_F32;
     p.inv_n = 1.0f / static_cast<float>(d->tokens);
@@ -114,6 +117,7 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
     a.d = d->head_dim;
     a.causal = d->causal != 0;
     a.out_f32 = d->out_dtype == SAB_F32;
+    a.per_token = d->qk_granularity == SAB_QK_PER_TOKEN;
     return a;
 }
 
@@ -181,6 +185,7 @@ void sab_desc_init(sab_desc* d, int32_t batch, int32_t heads, int32_t tokens, in
     d->smooth_k = 1;
     d->pv_accum = SAB_PV_FP32;
     d->check_v = 0;
+    d->qk_granularity = SAB_QK_PER_BLOCK;
 }
 
 int sab_check_desc(const sab_desc* d) {
@@ -193,7 +198,9 @@ int sab_check_desc(const sab_desc* d) {
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: head_dim must be 64 or 128 on the B200 path");
     if (d->block_q != kBlockQ || d->block_kv != kBlockKV)
         return set_error(SAB_ERR_UNSUPPORTED,
-                         "sage_attention: SAGEAttn-B uses block_q=128, block_kv=64 (kernel_config_for(B))");
+                         "sage_attention: SAGEAttn-B/T use block_q=128, block_kv=64 (kernel_config_for(B|T))");
+    if (d->qk_granularity != SAB_QK_PER_BLOCK && d->qk_granularity != SAB_QK_PER_TOKEN)
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: Q/K granularity must be per-block (B) or per-token (T)");
     if ((d->in_dtype != SAB_F16 && d->in_dtype != SAB_F32) || (d->out_dtype != SAB_F16 && d->out_dtype != SAB_F32))
         return set_error(SAB_ERR_ARGUMENT, "sab_desc: dtype must be SAB_F16 or SAB_F32");
     if (d->pv_accum != SAB_PV_FP32)

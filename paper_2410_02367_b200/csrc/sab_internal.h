@@ -35,6 +35,7 @@ struct PrepassParams {
     int nodes_per_cta;  // nodes summed per mean-partial CTA (power of two)
     int n_partials;     // 2^depth / nodes_per_cta
     int smooth;
+    int per_token;      // SAGEAttn-T: one scale per token (qscales/kscales [units][n])
     int check_v;
     int in_f32;
     float inv_n;        // 1.0f / float(N)          (quant.hpp:228)
@@ -57,7 +58,7 @@ struct AttnParams {
     void* o;
     int* status;
     int32_t* s_dump;  // debug: INT32 S tiles of one (unit, q-tile)
-    int units, n, d, causal, out_f32;
+    int units, n, d, causal, out_f32, per_token;
     int dump_unit, dump_qtile;
     int group_units;  // K2 raster: units per L2-resident group (set by launch_attention)
 };

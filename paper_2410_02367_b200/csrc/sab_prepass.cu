@@ -374,6 +374,72 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
     __syncthreads();
     mbar_wait(smem_u32(&bar), 0);
 
+    if (p.per_token) {
+        // SAGEAttn-T: Granularity::per_token (quant.hpp:37-63) -- one scale per row of
+        // folded Q and of smoothed K.  A row's 8-channel vectors sit on CV consecutive
+        // lanes, which reduce its two maxima by shuffles; then each lane writes its codes.
+        const int ngq = (p.n + kBlockKV - 1) / kBlockKV * kBlockKV;  // scale rows [units][npad], npad = 64*ceil(n/64)
+        bool finite = true;
+#pragma unroll 1
+        for (int i = 0; i < VPT; ++i) {
+            const int v = tid + i * kQThreads;
+            const int row = v / CV, col = (v % CV) * 8;
+            const bool valid = row < rows;
+            float q[8], k[8];
+            float aq = 0.0f, ak = 0.0f;
+            if (valid) {
+                load8<T>(sq + row * D + col, q);
+                load8<T>(sk + row * D + col, k);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    finite &= isfinite(q[e]) && isfinite(k[e]);
+                    q[e] = __fmul_rn(q[e], p.fold);
+                    k[e] = __fsub_rn(k[e], s_mean[col + e]);
+                    aq = fmaxf(aq, fabsf(q[e]));
+                    ak = fmaxf(ak, fabsf(k[e]));
+                }
+            }
+#pragma unroll
+            for (int o = CV / 2; o > 0; o >>= 1) {
+                aq = fmaxf(aq, __shfl_xor_sync(0xffffffffu, aq, o));
+                ak = fmaxf(ak, __shfl_xor_sync(0xffffffffu, ak, o));
+            }
+            if (valid) {
+                float dq, iq, dk, ik;
+                int8_scale(aq, dq, iq);
+                int8_scale(ak, dk, ik);
+                const size_t off = ubase + static_cast<size_t>(r0 + row) * D + col;
+                *reinterpret_cast<uint2*>(p.qcodes + off) = isinf(iq) ? codes8_fast<true>(q, iq) : codes8_fast<false>(q, iq);
+                *reinterpret_cast<uint2*>(p.kcodes + off) = isinf(ik) ? codes8_fast<true>(k, ik) : codes8_fast<false>(k, ik);
+                if (col == 0) {
+                    p.qscales[static_cast<size_t>(unit) * ngq + r0 + row] = dq;
+                    p.kscales[static_cast<size_t>(unit) * ngq + r0 + row] = dk;
+                }
+            }
+        }
+        if (!finite) atomicOr(p.status, kStatusNonFinite);
+        if (p.in_f32 || p.check_v) {
+            bool vfin = true;
+            for (int v = tid; v < rows * CV; v += kQThreads) {
+                const int row = v / CV, c8 = (v % CV) * 8;
+                const size_t off = ubase + static_cast<size_t>(r0 + row) * D + c8;
+                float x[8];
+                load8<T>(static_cast<const T*>(p.v) + off, x);
+                vfin &= all_finite8(x);
+                if (p.in_f32) {
+                    uint4 h;
+                    h.x = pack_half2(x[0], x[1]);
+                    h.y = pack_half2(x[2], x[3]);
+                    h.z = pack_half2(x[4], x[5]);
+                    h.w = pack_half2(x[6], x[7]);
+                    *reinterpret_cast<uint4*>(p.v16 + off) = h;
+                }
+            }
+            if (!vfin) atomicOr(p.status, kStatusNonFinite);
+        }
+        return;
+    }
+
     if constexpr (std::is_same<T, __half>::value) {
         // fp16 fast path.  Every thread keeps one 8-channel column block (CV divides
         // the thread count), so its eight K means live in registers.

@@ -62,7 +62,7 @@ int main(int argc, char** argv) {
     ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(nan_in, sageattn::SageVariant::B); },
                                         "non-finite input");
     ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(in, sageattn::SageVariant::VB); },
-                                        "SAGEAttn-B");
+                                        "SAGEAttn-B / SAGEAttn-T");
     ok &= sageattn::apply_causal_tiling(0, 2, 128, 64, 1000) == sageattn::TileKind::Skip;
     std::printf(ok ? "ERRORS OK\n" : "ERRORS FAILED\n");
     return ok ? 0 : 1;

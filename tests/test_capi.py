@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sab_abi_version() == 1
+    assert lib.sab_abi_version() == 2
 
 
 def test_desc_validation_mirrors_reference():
@@ -35,6 +35,17 @@ def test_desc_validation_mirrors_reference():
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, block_q=64))) == _lib.SAB_ERR_UNSUPPORTED
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=_lib.SAB_PV_FP16_TILE))) == \
         _lib.SAB_ERR_UNSUPPORTED
+    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, per_token=True))) == _lib.SAB_OK
+    bad_g = _lib.desc(1, 1, 1024, 64)
+    bad_g.qk_granularity = 2  # per-tensor is not a SAGEAttn variant
+    assert lib.sab_check_desc(C.byref(bad_g)) == _lib.SAB_ERR_UNSUPPORTED
+
+
+def test_per_token_layout_pads_scale_rows():
+    for n in (1, 63, 64, 1105):
+        L = _lib.workspace_layout(_lib.desc(2, 1, n, 64, per_token=True))
+        npad = -(-n // 64) * 64
+        assert L.kscales - L.qscales >= 2 * npad * 4 and L.mean_k - L.kscales >= 2 * npad * 4
 
 
 @pytest.mark.parametrize("n,depth", [(1, 0), (8, 0), (9, 1), (17, 1), (18, 2), (1024, 7), (8192, 10),
@@ -99,7 +110,7 @@ def test_python_mirror_validation_without_gpu():
         sageattn.sage_attention(sageattn.AttentionInput(q, q[:, :, :2], q), sageattn.SageVariant.B)
     with pytest.raises(ValueError, match="block sizes must be >= 1"):
         sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.KernelConfig(block_kv=0))
-    with pytest.raises(ValueError, match="SAGEAttn-B"):
+    with pytest.raises(ValueError, match="SAGEAttn-B / SAGEAttn-T"):
         sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.SageVariant.VB)
     assert sageattn.kernel_config_for(sageattn.SageVariant.B) == sageattn.KernelConfig()
     assert sageattn.apply_causal_tiling(0, 2, 128, 64, 1000) == sageattn.TileKind.Skip
