@@ -642,365 +642,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// ==================================================================== K2, 128-key ping-pong
-// SAGEAttn-B kernel with 128-key KV steps (two K quantization groups per step):
-//   * QK^T runs as one bias MMA + D/32 kind::i8 MMAs of N = 128, which read the Q^
-//     operand from SMEM once per 128 keys (the N = 64 MMAs were SMEM-bound at
-//     48 cycles, profiles/r01_micro_umma.txt) and reach the ideal 64-cycle rate;
-//   * S is single-buffered per query tile ([128x, +128) TMEM columns) with P in its
-//     first 64 columns, so QK_x(j+1) follows PV_x(j) on the tensor pipe and the two
-//     tiles ping-pong: tile A's softmax overlaps tile B's MMAs and vice versa;
-//   * softmax threads t < 16 / t >= 16 of a warp own keys [0, 64) / [64, 128) of a
-//     row, i.e. exactly one K scale group each.
-template <int D>
-struct CfgPP {
-    static constexpr int kKeys = 128;                       // keys per step
-    static constexpr int kStages = D == 128 ? 3 : 6;        // 128-key K^/V stages
-    static constexpr int kQBytes = kBM * D;
-    static constexpr int kKBytes = kKeys * D;
-    static constexpr int kVBytes = kKeys * D * 2;
-    static constexpr int kVChunk = kKeys * 64 * 2;          // one 64-column SW128 panel of V
-    static constexpr uint32_t kSwizzleQK = D == 128 ? kSwizzle128B : kSwizzle64B;
-    static constexpr uint32_t kSboQK = 8 * D;
-    static constexpr int kOffQ = 0;
-    static constexpr int kOffK = kOffQ + 2 * kQBytes;
-    static constexpr int kOffV = kOffK + kStages * kKBytes;
-    static constexpr int kOffBiasA = kOffV + kStages * kVBytes;  // 128 x 16 fp16 of 2048
-    static constexpr int kOffBiasB = kOffBiasA + 4096;           // 128 x 16 fp16 of 384
-    static constexpr int kOffBar = kOffBiasB + 4096;
-    static constexpr int kSmemBytes = kOffBar + 512 + 1024;
-};
-
-struct BarsPP {
-    uint64_t q_full;
-    uint64_t kv_full[8], kv_empty[8];
-    uint64_t s_full[2], p_full[2], pv_done[2], o_final[2];
-    uint32_t tmem_base;
-};
-
-// Softmax of one 128-key S row half (64 keys = one K group) per thread; see
-// softmax_half for the arithmetic.  P is written as 32 fp16x2 words into the first
-// 64 TMEM columns of the S tile (thread t < 16: columns [0, 32), t >= 16: [32, 64)).
-template <bool MASK>
-__device__ __forceinline__ float softmax_pp(const uint32_t (&r)[64], uint32_t ts, float cg, int lim, float& m, float& l,
-                                            bool& rescale) {
-    // The two halves of a row carry different K group scales, so their maxima meet
-    // as scaled floats.
-    const int imax = group_max<MASK>(r, lim);
-    float mx = (MASK && imax == kMaskedAcc) ? -INFINITY : (__int_as_float(imax) - kMagicF) * cg;
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-    const float m_new = fmaxf(m, mx);
-    rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
-    float alpha = 1.0f;
-    if (rescale) {
-        alpha = ex2(m - m_new);
-        m = m_new;
-    }
-    const float mref = (m == -INFINITY) ? 0.0f : m;
-    const f2 cg2{cg, cg};
-    const float bgs = -fmaf(kMagicF, cg, mref);
-    const f2 bg{bgs, bgs};
-    const int lim2 = MASK ? opaque(lim) : lim;
-    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-    uint32_t pk[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const int c = 2 * i;
-        const f2 t = ffma2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, cg2, bg);
-        f2 pp;
-        if ((c & 15) >= 16 - kPolyPer16) {
-            pp = exp2_poly2(t);
-        } else {
-            pp = f2{ex2(t.x), ex2(t.y)};
-        }
-        if (MASK) {
-            pp.x = (c >= lim2) ? 0.0f : pp.x;
-            pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
-        }
-        pk[i] = pack_half2(pp.x, pp.y);
-        acc[i & 3] = fadd2(acc[i & 3], pp);
-    }
-    tmem_st16x2_32o<32>(ts, pk);
-    const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-    l = fmaf(l, alpha, sum.x + sum.y);
-    return alpha;
-}
-
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP>
-__global__ void __launch_bounds__(kThreads, 1)
-    k2_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-          const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
-    using C = CfgPP<D>;
-    constexpr int S = C::kStages;
-    constexpr int KS = C::kKeys;
-    static_assert(sizeof(BarsPP) <= 512, "barrier block overflows its reservation");
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    BarsPP* bars = reinterpret_cast<BarsPP*>(smem + C::kOffBar);
-    const uint32_t sQ = smem_u32(smem + C::kOffQ);
-    const uint32_t sK = smem_u32(smem + C::kOffK);
-    const uint32_t sV = smem_u32(smem + C::kOffV);
-
-    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);
-    const int lane = threadIdx.x % 32;
-    const int n = p.n;
-    const int ntq = (n + kBM - 1) / kBM;
-    const int ntk = (n + kBN - 1) / kBN;    // 64-key K groups
-    const int nts = (n + KS - 1) / KS;      // 128-key steps
-    const int npair = (ntq + 1) / 2;
-
-    int unit, pair;
-    if (DUMP) {
-        unit = p.dump_unit;
-        pair = p.dump_qtile / 2;
-    } else {
-        const int gu = p.group_units;
-        const int g = static_cast<int>(blockIdx.x) / (gu * npair);
-        const int r = static_cast<int>(blockIdx.x) - g * gu * npair;
-        const int gsz = min(gu, p.units - g * gu);
-        unit = g * gu + r % gsz;
-        pair = npair - 1 - r / gsz;
-    }
-    const int qt0 = 2 * pair;
-    const bool has_b = qt0 + 1 < ntq;
-    // Causal: query tile qt (rows < 128(qt+1)) needs the 128-key steps j <= qt.
-    const int nkv_a = CAUSAL ? min(qt0 + 1, nts) : nts;
-    const int nkv_b = has_b ? (CAUSAL ? min(qt0 + 2, nts) : nts) : 0;
-    const int nkv = max(nkv_a, nkv_b);
-
-    {
-        uint4* bias = reinterpret_cast<uint4*>(smem + C::kOffBiasA);
-        const uint4 a2048 = make_uint4(0x68006800u, 0x68006800u, 0x68006800u, 0x68006800u);
-        const uint4 b384 = make_uint4(0x5E005E00u, 0x5E005E00u, 0x5E005E00u, 0x5E005E00u);
-        for (int i = threadIdx.x; i < 8192 / 16; i += kThreads) bias[i] = i < 4096 / 16 ? a2048 : b384;
-        fence_proxy_async_smem();
-    }
-    if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&bars->q_full), 1);
-        for (int s = 0; s < S; ++s) {
-            mbar_init(smem_u32(&bars->kv_full[s]), 1);
-            mbar_init(smem_u32(&bars->kv_empty[s]), 1);
-        }
-        for (int x = 0; x < 2; ++x) {
-            mbar_init(smem_u32(&bars->s_full[x]), 1);
-            mbar_init(smem_u32(&bars->p_full[x]), 8);  // one arrival per softmax warp of the tile
-            mbar_init(smem_u32(&bars->pv_done[x]), 1);
-            mbar_init(smem_u32(&bars->o_final[x]), 1);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 16) tmem_alloc<512>(smem_u32(&bars->tmem_base));
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tbase = bars->tmem_base;
-
-    if (warp == 16) {
-        // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            tma_prefetch_desc(&tm_q);
-            tma_prefetch_desc(&tm_k);
-            tma_prefetch_desc(&tm_v);
-            mbar_arrive_expect_tx(smem_u32(&bars->q_full), (has_b ? 2 : 1) * C::kQBytes);
-            tma_load_3d(sQ, &tm_q, smem_u32(&bars->q_full), 0, qt0 * kBM, unit);
-            if (has_b) tma_load_3d(sQ + C::kQBytes, &tm_q, smem_u32(&bars->q_full), 0, (qt0 + 1) * kBM, unit);
-            for (int j = 0; j < nkv; ++j) {
-                const int s = j % S;
-                mbar_wait(smem_u32(&bars->kv_empty[s]), ((j / S) & 1) ^ 1);
-                const uint32_t full = smem_u32(&bars->kv_full[s]);
-                mbar_arrive_expect_tx(full, C::kKBytes + C::kVBytes);
-                tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, j * KS, unit);
-#pragma unroll
-                for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, j * KS, unit);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 17) {
-        // ------------------------------------------------------------ MMA issuer (both tiles)
-        // Per step j: PV_A(j), QK_A(j+1), PV_B(j), QK_B(j+1) -- each QK into the S buffer
-        // its tile's PV has just read (in-order tensor pipe).
-        constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, KS);
-        constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
-        constexpr uint32_t idesc_bias = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 0, kBM, KS);
-        const uint64_t dq0 = make_smem_desc(sQ, 16, C::kSboQK, C::kSwizzleQK);
-        const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
-        const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
-        const uint64_t d_bias_a = make_smem_desc(smem_u32(smem + C::kOffBiasA), 128, 256, kSwizzleNone);
-        const uint64_t d_bias_b = make_smem_desc(smem_u32(smem + C::kOffBiasB), 128, 256, kSwizzleNone);
-        auto issue_qk = [&](int x, int j) {
-            const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
-            const uint64_t dk = dk0 + static_cast<uint64_t>(((j % S) * C::kKBytes) >> 4);
-            const uint32_t t_s = tbase + x * 128;
-            if (elect_one()) {
-                umma_f16_ss(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
-#pragma unroll
-                for (int kk = 0; kk < D / 32; ++kk)
-                    umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2), idesc_qk,
-                               1u);
-                umma_commit(smem_u32(&bars->s_full[x]));
-            }
-            __syncwarp();
-        };
-        auto wait_kv = [&](int j) {
-            mbar_wait(smem_u32(&bars->kv_full[j % S]), (j / S) & 1);
-            tc_fence_after();
-        };
-        if (nkv > 0) {
-            mbar_wait(smem_u32(&bars->q_full), 0);
-            wait_kv(0);
-            if (nkv_a > 0) issue_qk(0, 0);
-            if (nkv_b > 0) issue_qk(1, 0);
-        }
-        for (int j = 0; j < nkv; ++j) {
-            const int s = j % S;
-            bool kv_ready = false;
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-                const int nkv_x = x == 0 ? nkv_a : nkv_b;
-                if (j < nkv_x) {
-                    mbar_wait(smem_u32(&bars->p_full[x]), j & 1);
-                    tc_fence_after();
-                    const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
-                    const uint32_t t_p = tbase + x * 128;
-                    const uint32_t t_o = tbase + 256 + x * D;
-                    if (elect_one()) {
-#pragma unroll
-                        for (int kk = 0; kk < KS / 16; ++kk)
-                            umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
-                                        (j > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit(smem_u32(&bars->pv_done[x]));
-                        if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
-                    }
-                    __syncwarp();
-                }
-                if (x == 1) {
-                    if (elect_one()) umma_commit(smem_u32(&bars->kv_empty[s]));
-                    __syncwarp();
-                }
-                if (j + 1 < nkv_x) {
-                    if (!kv_ready) wait_kv(j + 1);
-                    kv_ready = true;
-                    issue_qk(x, j + 1);
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp < 16) {
-        // ------------------------------------------------------------ softmax warpgroups
-        // Tile x = warp / 8; warp w covers TMEM lanes [32(w%4) + 16((w%8)/4), +16); its
-        // threads t and t + 16 share one query row and own keys [0, 64) / [64, 128)
-        // of each step, one K scale group each.
-        const int x = warp / 8;
-        const int qt = qt0 + x;
-        const int nkv_x = x == 0 ? nkv_a : nkv_b;
-        const int lane_base = (warp % 4) * 32 + ((warp % 8) / 4) * 16;
-        const int half = lane / 16;
-        const int row = lane_base + (lane % 16);
-        const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
-        const uint32_t t_s = tbase + lane_off + x * 128;
-        const uint32_t t_o = tbase + lane_off + 256 + x * D;
-        const int qi = qt * kBM + row;
-        float m = -INFINITY, l = 0.0f;
-        if (nkv_x > 0) {
-            const float qsl = p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
-            const float* ksc = p.kscales + static_cast<size_t>(unit) * ntk;
-            float ks_next = (half < ntk) ? __ldg(ksc + half) : 1.0f;
-            for (int j = 0; j < nkv_x; ++j) {
-                const float ks_cur = ks_next;
-                const int gn = 2 * (j + 1) + half;
-                if (j + 1 < nkv_x) ks_next = gn < ntk ? __ldg(ksc + gn) : 1.0f;
-                mbar_wait(smem_u32(&bars->s_full[x]), j & 1);
-                tc_fence_after();
-                uint32_t r[64];
-                tmem_ld16x2_64o<64>(t_s, r);
-                tmem_wait_ld();
-                const int kb = j * KS + 64 * half;  // first key of this thread's half
-                if (DUMP && qt == p.dump_qtile && 2 * j + half < ntk) {
-                    int32_t* dump = p.s_dump + (static_cast<size_t>(2 * j + half) * kBM + row) * kBN;
-#pragma unroll
-                    for (int c = 0; c < 64; c += 4)
-                        *reinterpret_cast<int4*>(dump + c) = make_int4(r[c] - kMagicI, r[c + 1] - kMagicI,
-                                                                       r[c + 2] - kMagicI, r[c + 3] - kMagicI);
-                }
-                const float cg = qsl * ks_cur;
-                const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb;
-                const bool need_mask = (j * KS + KS > n) || (CAUSAL && j * KS + KS - 1 > qt * kBM);
-                bool rescale;
-                float alpha;
-                if (need_mask)
-                    alpha = softmax_pp<true>(r, t_s, cg, lim, m, l, rescale);
-                else
-                    alpha = softmax_pp<false>(r, t_s, cg, lim, m, l, rescale);
-                if (rescale && j > 0) {
-                    // PV_x(j-1) must have finished accumulating into O_x; PV_x(j) needs this
-                    // step's P, so parity (j-1)&1 is unambiguous.
-                    mbar_wait(smem_u32(&bars->pv_done[x]), (j - 1) & 1);
-                    tc_fence_after();
-#pragma unroll 1
-                    for (int c = 0; c < D / 2; c += 32) {
-                        uint32_t o[32];
-                        tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                        tmem_st16x2_32o<D / 2>(t_o + c, o);
-                    }
-                }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x]));
-            }
-
-            // -------------------------------------------------------- epilogue
-            mbar_wait(smem_u32(&bars->o_final[x]), 0);
-            tc_fence_after();
-            l += __shfl_xor_sync(0xffffffffu, l, 16);
-            if (!DUMP) {
-                const float inv_l = 1.0f / l;
-                bool finite = true;
-#pragma unroll 1
-                for (int c = 0; c < D / 2; c += 32) {
-                    uint32_t o[32];
-                    tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                    tmem_wait_ld();
-                    float v[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        finite &= isfinite(__uint_as_float(o[e]));
-                        v[e] = __uint_as_float(o[e]) * inv_l;
-                    }
-                    if (qi < n) {
-                        const size_t off = (static_cast<size_t>(unit) * n + qi) * D + half * (D / 2) + c;
-                        if (OUT_F32) {
-                            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
-#pragma unroll
-                            for (int e = 0; e < 8; ++e)
-                                dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                        } else {
-                            uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
-                                                    pack_half2(v[8 * e + 4], v[8 * e + 5]),
-                                                    pack_half2(v[8 * e + 6], v[8 * e + 7]));
-                        }
-                    }
-                }
-                if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
-            }
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 16) {
-        tc_fence_after();
-        tmem_dealloc<512>(tbase);
-    }
-}
-
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1085,48 +726,8 @@ cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
 }
 
 // The INT32 S dump does not read the scales, so it only needs the per-block build.
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP>
-cudaError_t launch_pp(const AttnParams& p, cudaStream_t s) {
-    using C = CfgPP<D>;
-    CUtensorMap tq, tk, tv;
-    const CUtensorMapSwizzle swqk = D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    if (!make_map(&tq, p.qcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBM, swqk) ||
-        !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, C::kKeys, swqk) ||
-        !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, C::kKeys,
-                  CU_TENSOR_MAP_SWIZZLE_128B))
-        return cudaErrorInvalidValue;
-    AttnParams pp = p;
-    pp.group_units = raster_group_units(p, D);
-    auto kern = k2_pp<D, CAUSAL, OUT_F32, DUMP>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    const int ntq = (p.n + kBM - 1) / kBM;
-    const unsigned grid = DUMP ? 1u : static_cast<unsigned>((ntq + 1) / 2) * static_cast<unsigned>(p.units);
-    kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, pp);
-    return cudaGetLastError();
-}
-
-#ifndef SAB_K2_PP
-#define SAB_K2_PP 0
-#endif
-
-template <bool DUMP>
-cudaError_t dispatch_pp(const AttnParams& p, cudaStream_t s) {
-    const bool c = p.causal != 0, f = p.out_f32 != 0;
-    if (p.d == 128) {
-        if (c) return f ? launch_pp<128, true, true, DUMP>(p, s) : launch_pp<128, true, false, DUMP>(p, s);
-        return f ? launch_pp<128, false, true, DUMP>(p, s) : launch_pp<128, false, false, DUMP>(p, s);
-    }
-    if (p.d == 64) {
-        if (c) return f ? launch_pp<64, true, true, DUMP>(p, s) : launch_pp<64, true, false, DUMP>(p, s);
-        return f ? launch_pp<64, false, true, DUMP>(p, s) : launch_pp<64, false, false, DUMP>(p, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
 template <bool DUMP>
 cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
-    if (SAB_K2_PP && !p.per_token) return dispatch_pp<DUMP>(p, s);
     if (!DUMP && p.per_token) return dispatch_pt<false, true>(p, s);
     return dispatch_pt<DUMP, false>(p, s);
 }
