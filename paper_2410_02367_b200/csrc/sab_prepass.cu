@@ -8,11 +8,14 @@
 //                       cvt.rn.f16.f32 == round_to_half for finite floats)
 //
 // Two launches per call:
-//   k1_mean_partials  grid (n_partials, units): each CTA sums an aligned
-//                     subtree of 'nodes_per_cta' leaf-level nodes of the
-//                     reference's pairwise tree for all head_dim channels;
-//                     the last CTA of each unit (per-unit counter) then sums
-//                     the top of the tree over the CTA partials -> mean_k.
+//   fp16 inputs, per-block scales (the SAGEAttn-B bench and fp16 drop-in path):
+//     k1_mean_and_q   grid (n_partials + ceil(N/128), units): mean-tree partials of
+//                     K (the last CTA of each unit, found by a per-unit counter,
+//                     sums the top of the tree -> mean_k) next to Q fold+quantize
+//                     chunks, which do not need mean_k;
+//     k1_k_fast       grid (ceil(N/128), units): smooth + quantize K.
+//   otherwise (fp32 inputs, per-token scales, smoothing off):
+//     k1_mean_partials  grid (n_partials, units): the same mean tree;
 //   k1_quantize       grid (ceil(N/128), units): reads mean_k, then quantizes
 //                     one 128-token Q group and the two 64-token K groups of
 //                     that chunk.
@@ -172,13 +175,11 @@ __device__ __forceinline__ void mean_top(const PrepassParams& p, int unit, int c
 }
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
+__device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, int chunk) {
     constexpr int CV = D / 8;           // 8-channel vectors per row
     constexpr int NG = kThreads / CV;   // node groups per CTA
     __shared__ float red[NG][D];
 
-    const int unit = blockIdx.y;
-    const int chunk = blockIdx.x;
     const int cv = threadIdx.x % CV;
     const int grp = threadIdx.x / CV;
     const int active = p.nodes_per_cta / G;  // groups holding G nodes each
@@ -240,6 +241,11 @@ __global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
         __threadfence();
         if (threadIdx.x < D) mean_top<D>(p, unit, threadIdx.x);
     }
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
+    mean_partial<T, D, G>(p, blockIdx.y, blockIdx.x);
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -630,9 +636,208 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
     }
 }
 
+// ---- fp16, per-block fast path in two launches (SAGEAttn-B bench / drop-in fp16 path):
+//   k1_mean_and_q  grid (n_partials + ceil(N/128), units): CTAs [0, n_partials) are the
+//                  mean-tree partials of K (last CTA sums the top), the others fold and
+//                  quantize one 128-token Q chunk -- Q does not need mean(K), so K's
+//                  reduction and Q's quantization share one pass over HBM;
+//   k1_k_fast      grid (ceil(N/128), units): smooth + quantize the two 64-token K groups
+//                  of a chunk once mean(K) is known (K is re-read, mostly from L2).
+template <int D>
+__device__ __forceinline__ void q_chunk_fast(const PrepassParams& p, int unit, int chunk, uint8_t* smem) {
+    constexpr int CV = D / 8;
+    constexpr int VPT = kBlockQ * CV / kQThreads;
+    const __half* sq = reinterpret_cast<const __half*>(smem);
+    __shared__ uint64_t bar;
+    __shared__ float s_red[kQThreads / 32];
+    __shared__ float s_inv;
+    const int tid = threadIdx.x;
+    const int r0 = chunk * kBlockQ;
+    const int rows = min(kBlockQ, p.n - r0);
+    const size_t ubase = static_cast<size_t>(unit) * p.n * D;
+    const uint32_t bytes = static_cast<uint32_t>(rows) * D * 2;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(smem_u32(&bar), bytes);
+        bulk_load(smem_u32(smem), static_cast<const __half*>(p.q) + ubase + static_cast<size_t>(r0) * D, bytes,
+                  smem_u32(&bar));
+    }
+    __syncthreads();
+    mbar_wait(smem_u32(&bar), 0);
+    const int col = (tid % CV) * 8;
+    // max|fl(q * fold)| = fl(max|q| * fold); max|q| as a 16-bit max over sign-cleared bits,
+    // which also flags inf / NaN (>= 0x7C00).
+    uint32_t qbits = 0;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int row = (tid + i * kQThreads) / CV;
+        if (row < rows) {
+            const uint4 u = *reinterpret_cast<const uint4*>(sq + row * D + col);
+            qbits = __vmaxu2(__vmaxu2(qbits, u.x & 0x7FFF7FFFu), u.y & 0x7FFF7FFFu);
+            qbits = __vmaxu2(__vmaxu2(qbits, u.z & 0x7FFF7FFFu), u.w & 0x7FFF7FFFu);
+        }
+    }
+    const uint32_t qb = max(qbits & 0xFFFFu, qbits >> 16);
+    if (qb >= 0x7C00u) atomicOr(p.status, kStatusNonFinite);
+    float amax = warp_max(__fmul_rn(__half2float(__ushort_as_half(static_cast<unsigned short>(qb))), p.fold));
+    if ((tid & 31) == 0) s_red[tid >> 5] = amax;
+    __syncthreads();
+    if (tid == 0) {
+        float m = 0.0f;
+        for (int w = 0; w < kQThreads / 32; ++w) m = fmaxf(m, s_red[w]);
+        float delta, inv;
+        int8_scale(m, delta, inv);
+        s_inv = inv;
+        p.qscales[static_cast<size_t>(unit) * ((p.n + kBlockQ - 1) / kBlockQ) + chunk] = delta;
+    }
+    __syncthreads();
+    const float iq = s_inv;
+    const bool clamp = isinf(iq);
+    const f2 fold2{p.fold, p.fold}, iq2{iq, iq};
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int row = (tid + i * kQThreads) / CV;
+        if (row < rows) {
+            const uint4 u = *reinterpret_cast<const uint4*>(sq + row * D + col);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            f2 t[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) t[e] = mul2(mul2(h2f(w[e]), fold2), iq2);
+            *reinterpret_cast<uint2*>(p.qcodes + ubase + static_cast<size_t>(r0 + row) * D + col) =
+                clamp ? pack_codes8<true>(t) : pack_codes8<false>(t);
+        }
+    }
+}
+
+#ifndef SAB_K1_MINB
+#define SAB_K1_MINB 4  // <= 64 registers: more Q-chunk CTAs in flight (C2 K1 78 -> 68 us)
+#endif
+template <int D, int G>
+__global__ void __launch_bounds__(kQThreads, SAB_K1_MINB) k1_mean_and_q(PrepassParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    if (static_cast<int>(blockIdx.x) < p.n_partials) mean_partial<__half, D, G>(p, blockIdx.y, blockIdx.x);
+    else q_chunk_fast<D>(p, blockIdx.y, blockIdx.x - p.n_partials, smem);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
+    constexpr int CV = D / 8;
+    constexpr int VPT = kBlockQ * CV / kQThreads;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const __half* sk = reinterpret_cast<const __half*>(smem);
+    __shared__ uint64_t bar;
+    __shared__ float s_mean[D];
+    __shared__ float s_red[kQThreads / 32][2];
+    __shared__ float s_inv[2];
+    const int unit = blockIdx.y, chunk = blockIdx.x, tid = threadIdx.x;
+    const int r0 = chunk * kBlockQ;
+    const int rows = min(kBlockQ, p.n - r0);
+    const size_t ubase = static_cast<size_t>(unit) * p.n * D;
+    const uint32_t bytes = static_cast<uint32_t>(rows) * D * 2;
+    if (tid == 0) {
+        mbar_init(smem_u32(&bar), 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(smem_u32(&bar), bytes);
+        bulk_load(smem_u32(smem), static_cast<const __half*>(p.k) + ubase + static_cast<size_t>(r0) * D, bytes,
+                  smem_u32(&bar));
+    }
+    if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
+    __syncthreads();
+    mbar_wait(smem_u32(&bar), 0);
+    const int col = (tid % CV) * 8;
+    f2 mc[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) mc[w] = f2{-s_mean[col + 2 * w], -s_mean[col + 2 * w + 1]};
+    uint32_t kbits = 0;
+    float amax0 = 0.0f, amax1 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int row = (tid + i * kQThreads) / CV;
+        if (row < rows) {
+            const uint4 u = *reinterpret_cast<const uint4*>(sk + row * D + col);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            float a = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                kbits = __vmaxu2(kbits, w[e] & 0x7FFF7FFFu);
+                const f2 d = add2(h2f(w[e]), mc[e]);
+                a = fmaxf(a, fmaxf(fabsf(d.x), fabsf(d.y)));
+            }
+            if (i < VPT / 2) amax0 = fmaxf(amax0, a);
+            else amax1 = fmaxf(amax1, a);
+        }
+    }
+    if (max(kbits & 0xFFFFu, kbits >> 16) >= 0x7C00u) atomicOr(p.status, kStatusNonFinite);
+    amax0 = warp_max(amax0);
+    amax1 = warp_max(amax1);
+    if ((tid & 31) == 0) {
+        s_red[tid >> 5][0] = amax0;
+        s_red[tid >> 5][1] = amax1;
+    }
+    __syncthreads();
+    if (tid < 2) {
+        float m = 0.0f;
+        for (int w = 0; w < kQThreads / 32; ++w) m = fmaxf(m, s_red[w][tid]);
+        float delta, inv;
+        int8_scale(m, delta, inv);
+        s_inv[tid] = inv;
+        const int ngk = (p.n + kBlockKV - 1) / kBlockKV;
+        const int g = 2 * chunk + tid;
+        if (g < ngk) p.kscales[static_cast<size_t>(unit) * ngk + g] = delta;
+    }
+    __syncthreads();
+    const float ik0 = s_inv[0], ik1 = s_inv[1];
+    const bool clamp = isinf(ik0) || isinf(ik1);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int row = (tid + i * kQThreads) / CV;
+        if (row < rows) {
+            const uint4 u = *reinterpret_cast<const uint4*>(sk + row * D + col);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            const float ik = i < VPT / 2 ? ik0 : ik1;
+            const f2 ik2{ik, ik};
+            f2 t[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) t[e] = mul2(add2(h2f(w[e]), mc[e]), ik2);
+            *reinterpret_cast<uint2*>(p.kcodes + ubase + static_cast<size_t>(r0 + row) * D + col) =
+                clamp ? pack_codes8<true>(t) : pack_codes8<false>(t);
+        }
+    }
+    if (p.check_v) {
+        bool vfin = true;
+        for (int v = tid; v < rows * CV; v += kQThreads) {
+            const int row = v / CV, c8 = (v % CV) * 8;
+            float x[8];
+            load8<__half>(static_cast<const __half*>(p.v) + ubase + static_cast<size_t>(r0 + row) * D + c8, x);
+            vfin &= all_finite8(x);
+        }
+        if (!vfin) atomicOr(p.status, kStatusNonFinite);
+    }
+}
+
 template <typename T, int D>
 cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
+    if (std::is_same<T, __half>::value && p.smooth && !p.per_token) {
+        const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
+        constexpr int smem = kBlockQ * D * 2;
+        const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
+        cudaError_t e;
+        if (g == 1) {
+            e = cudaFuncSetAttribute(k1_mean_and_q<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess) k1_mean_and_q<D, 1><<<dim3(p.n_partials + ntq, p.units), kQThreads, smem, s>>>(p);
+        } else {
+            e = cudaFuncSetAttribute(k1_mean_and_q<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess) k1_mean_and_q<D, 2><<<dim3(p.n_partials + ntq, p.units), kQThreads, smem, s>>>(p);
+        }
+        if (e != cudaSuccess) return e;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k1_k_fast<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        k1_k_fast<D><<<dim3(ntq, p.units), kQThreads, smem, s>>>(p);
+        return cudaGetLastError();
+    }
     if (p.smooth) {
         const dim3 grid(p.n_partials, p.units);
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
