@@ -6,6 +6,12 @@ compiled from /root/reference/proj/include by oracle/Makefile).
 Each fixture holds the fp16 inputs and the reference's outputs: mean_k,
 Q^/K^ codes and per-block scales, O of sage_attention(B) for both P~V arms,
 the SageDiagnostics MAC counters and naive_attention's exact O.
+
+The t_*.npz fixtures (SAGEAttn-T) hold the per-token codes and
+scales (quantize(..., Granularity::per_token())) and O of
+sage_attention(in, SageVariant::T) for both arms:
+
+    python tests/golden/make_golden.py --variant-t
 """
 import os
 import sys
@@ -26,6 +32,25 @@ CASES = [
 ]
 
 
+T_CASES = [
+    ("t_small", 1, 2, 300, 64, False, "normal"),
+    ("t_causal_outlier_d128", 1, 1, 257, 128, True, "outlier"),
+]
+
+
+def main_t():
+    ref = Reference()
+    for name, b, h, n, d, causal, dist in T_CASES:
+        q, k, v = (x.reshape(b, h, n, d) for x in synth.qkv(b * h, n, d, dtype=np.float16, dist=dist))
+        q32, k32, v32 = (x.astype(np.float32) for x in (q, k, v))
+        qc, qs, kc, ks = ref.quantize_per_token(q32, k32)
+        o16 = ref.sage_attention_variant(q32, k32, v32, "T", causal, pv_fp32=False)
+        o32 = ref.sage_attention_variant(q32, k32, v32, "T", causal, pv_fp32=True)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), q=q, k=k, v=v, causal=causal, qcodes=qc, qscales=qs,
+                            kcodes=kc, kscales=ks, o_fp16acc=o16, o_fp32acc=o32)
+        print(name, "written")
+
+
 def main():
     ref = Reference()
     for name, b, h, n, d, causal, dist in CASES:
@@ -44,4 +69,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--variant-t" in sys.argv:
+        main_t()
+    else:
+        main()

@@ -6,6 +6,9 @@ relative L1 <= 2e-3 of O against the reference's FP32-accumulator arm
 (SageOptions::pv_fp32_accumulator, attention.hpp:454-471); error against
 the default FP16 arm and against exact attention is reported, not gated.
 """
+import glob
+import os
+
 import numpy as np
 import pytest
 
@@ -201,3 +204,29 @@ def test_host_path_many_chunks_equals_device_path(cuda):
     qd, kd, vd = (torch.from_numpy(x).cuda() for x in (q, k, v))
     od = sage_attention_cuda(qd, kd, vd, causal=False, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(oh, od)
+
+
+GOLDEN_B = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+                  if not os.path.basename(p).startswith("t_"))
+
+
+@pytest.mark.parametrize("path", GOLDEN_B, ids=[os.path.basename(p) for p in GOLDEN_B])
+def test_against_reference_fixtures(cuda, path):
+    """K1 bit-exact and O within tolerance against vectors produced by the reference itself."""
+    import torch
+
+    from paper_2410_02367_b200 import prepass_cuda, prepass_outputs, sage_attention_cuda
+
+    g = np.load(path)
+    b, h, n, d = g["q"].shape
+    qd, kd, vd = (torch.from_numpy(g[x]).to(cuda) for x in ("q", "k", "v"))
+    got = {key: t.cpu().numpy() for key, t in prepass_outputs(prepass_cuda(qd, kd)).items()}
+    assert np.array_equal(got["qcodes"], g["qcodes"].reshape(b * h, n, d))
+    assert np.array_equal(got["kcodes"], g["kcodes"].reshape(b * h, n, d))
+    assert np.array_equal(got["qscales"].view(np.uint32), g["qscales"].view(np.uint32))
+    assert np.array_equal(got["kscales"].view(np.uint32), g["kscales"].view(np.uint32))
+    assert np.array_equal(got["mean"].view(np.uint32), g["mean"].reshape(b * h, d).view(np.uint32))
+    o = sage_attention_cuda(qd, kd, vd, causal=bool(g["causal"]), out_dtype=torch.float32).cpu().numpy()
+    o, ref = o.reshape(-1, n, d), g["o_fp32acc"].reshape(-1, n, d)
+    cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
+    assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)

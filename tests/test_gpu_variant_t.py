@@ -6,6 +6,9 @@ against the oracle, which tests/test_oracle.py pins to the compiled reference
 tiles of the T codes are bit-exact.  O within the north-star tolerance of the
 reference's FP32-accumulator arm of variant T.
 """
+import glob
+import os
+
 import numpy as np
 import pytest
 
@@ -132,3 +135,28 @@ def test_dropin_variant_t(cuda, oracle):
     for variant in (SageVariant.VT, SageVariant.VB):
         with pytest.raises(ValueError):
             sage_attention(AttentionInput(q, k, v), variant)
+
+
+GOLDEN_T = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "t_*.npz")))
+
+
+@pytest.mark.parametrize("path", GOLDEN_T, ids=[os.path.basename(p) for p in GOLDEN_T])
+def test_per_token_against_reference_fixtures(cuda, path):
+    """K1 per-token codes/scales bit-exact and O within tolerance against vectors the reference produced."""
+    import torch
+
+    from paper_2410_02367_b200 import prepass_cuda, prepass_outputs, sage_attention_cuda
+
+    g = np.load(path)
+    b, h, n, d = g["q"].shape
+    qd, kd, vd = (torch.from_numpy(g[x]).to(cuda) for x in ("q", "k", "v"))
+    ws = prepass_cuda(qd, kd, per_token=True)
+    got = {key: t.cpu().numpy() for key, t in prepass_outputs(ws).items()}
+    assert np.array_equal(got["qcodes"], g["qcodes"].reshape(b * h, n, d))
+    assert np.array_equal(got["kcodes"], g["kcodes"].reshape(b * h, n, d))
+    assert np.array_equal(np.ascontiguousarray(got["qscales"]).view(np.uint32), g["qscales"].view(np.uint32))
+    assert np.array_equal(np.ascontiguousarray(got["kscales"]).view(np.uint32), g["kscales"].view(np.uint32))
+    o = sage_attention_cuda(qd, kd, vd, causal=bool(g["causal"]), out_dtype=torch.float32, per_token=True)
+    o, ref = o.cpu().numpy().reshape(-1, n, d), g["o_fp32acc"].reshape(-1, n, d)
+    cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
+    assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)
