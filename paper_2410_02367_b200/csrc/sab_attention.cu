@@ -642,286 +642,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// ==================================================================== K2 on CTA pairs (d = 128)
-// Same pipeline as k2_attention, but a cluster of two CTAs on one TPC shares each MMA
-// (tcgen05 cta_group::2, M = 256): the leader (rank 0) issues for both, the A operand
-// (Q^, bias, P) comes from each CTA's own SMEM/TMEM rows, and the B operand is split by N
-// across the pair -- K^ keys [0, 32) / [32, 64) of every 64-key tile, V channels
-// [0, 64) / [64, 128).  Per SM that halves the K^/V TMA traffic and the B-operand SMEM
-// reads, the bound of the single-CTA kernel (profiles/r01_experiments.md).
-// CTA r of the pair owns query tiles 4P + 2r (slot A) and 4P + 2r + 1 (slot B).
-#ifndef SAB_PAIR_STAGES
-#define SAB_PAIR_STAGES 10
-#endif
-struct CfgPair {
-    static constexpr int D = 128;
-    static constexpr int kStages = SAB_PAIR_STAGES;
-    static constexpr int kQBytes = kBM * D;          // one 128-row Q^ tile
-    static constexpr int kKBytes = 32 * D;           // this CTA's 32 keys of a K^ tile
-    static constexpr int kVBytes = kBN * 64 * 2;     // this CTA's 64 channels of a V tile (one SW128 panel)
-    static constexpr int kOffQ = 0;
-    static constexpr int kOffK = kOffQ + 2 * kQBytes;
-    static constexpr int kOffV = kOffK + kStages * kKBytes;
-    static constexpr int kOffBiasA = kOffV + kStages * kVBytes;  // 128 x 16 fp16 of 2048
-    static constexpr int kOffBiasB = kOffBiasA + 4096;           // 32 x 16 fp16 of 384 (+ slack)
-    static constexpr int kOffBar = kOffBiasB + 4096;
-    static constexpr int kSmemBytes = kOffBar + 512 + 1024;
-};
-static_assert(CfgPair::kStages <= 16, "Bars holds 16 K^/V stages");
-
-template <bool CAUSAL, bool OUT_F32>
-__global__ void __launch_bounds__(kThreads, 1)
-    k2_pair(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-            const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
-    using C = CfgPair;
-    constexpr int D = C::D;
-    constexpr int S = C::kStages;
-    static_assert(sizeof(Bars) <= 512, "barrier block overflows its reservation");
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
-    const uint32_t sQ = smem_u32(smem + C::kOffQ);
-    const uint32_t sK = smem_u32(smem + C::kOffK);
-    const uint32_t sV = smem_u32(smem + C::kOffV);
-
-    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);
-    const int lane = threadIdx.x % 32;
-    const uint32_t rank = cluster_rank();
-    const bool leader = rank == 0;
-    const int n = p.n;
-    const int ntq = (n + kBM - 1) / kBM;
-    const int ntk = (n + kBN - 1) / kBN;
-    const int nquad = (ntq + 3) / 4;
-
-    // Raster over clusters as in k2_attention (unit groups sized to L2, longest first).
-    const int cl = static_cast<int>(blockIdx.x) / 2;
-    const int gu = p.group_units;
-    const int g = cl / (gu * nquad);
-    const int rr = cl - g * gu * nquad;
-    const int gsz = min(gu, p.units - g * gu);
-    const int unit = g * gu + rr % gsz;
-    const int quad = nquad - 1 - rr / gsz;
-    // Both CTAs run the same KV tiles per slot: those the pair's later tile needs.
-    const int nkv_a = CAUSAL ? min(2 * (4 * quad + 2) + 2, ntk) : ntk;
-    const int nkv_b = CAUSAL ? min(2 * (4 * quad + 3) + 2, ntk) : ntk;
-    const int nkv = max(nkv_a, nkv_b);
-    const int qt0 = 4 * quad + 2 * static_cast<int>(rank);
-
-    {
-        uint4* bias = reinterpret_cast<uint4*>(smem + C::kOffBiasA);
-        const uint4 a2048 = make_uint4(0x68006800u, 0x68006800u, 0x68006800u, 0x68006800u);
-        const uint4 b384 = make_uint4(0x5E005E00u, 0x5E005E00u, 0x5E005E00u, 0x5E005E00u);
-        for (int i = threadIdx.x; i < 8192 / 16; i += kThreads) bias[i] = i < 4096 / 16 ? a2048 : b384;
-        fence_proxy_async_smem();
-    }
-    if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&bars->q_full), 1);
-        for (int s2 = 0; s2 < S; ++s2) {
-            mbar_init(smem_u32(&bars->kv_full[s2]), 1);
-            mbar_init(smem_u32(&bars->kv_empty[s2]), 1);
-        }
-        for (int x = 0; x < 2; ++x) {
-            for (int b = 0; b < 2; ++b) {
-                mbar_init(smem_u32(&bars->s_full[x][b]), 1);
-                mbar_init(smem_u32(&bars->p_full[x][b]), 16);  // 8 softmax warps per CTA, both CTAs
-            }
-            mbar_init(smem_u32(&bars->pv_done[x]), 1);
-            mbar_init(smem_u32(&bars->o_final[x]), 1);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 16) tmem_alloc_pair<512>(smem_u32(&bars->tmem_base));
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync_all();  // barrier inits visible to the peer before any remote arrival / TMA
-    tc_fence_after();
-    const uint32_t tbase = bars->tmem_base;
-
-    if (warp == 16) {
-        // ------------------------------------------------------------ TMA producer (both CTAs)
-        if (lane == 0) {
-            tma_prefetch_desc(&tm_q);
-            tma_prefetch_desc(&tm_k);
-            tma_prefetch_desc(&tm_v);
-            const uint32_t q_full = map_to_rank(smem_u32(&bars->q_full), 0);
-            if (leader) mbar_arrive_expect_tx(smem_u32(&bars->q_full), 4 * C::kQBytes);
-            tma_load_3d_pair(sQ, &tm_q, q_full, 0, qt0 * kBM, unit);
-            tma_load_3d_pair(sQ + C::kQBytes, &tm_q, q_full, 0, (qt0 + 1) * kBM, unit);
-            for (int j = 0; j < nkv; ++j) {
-                const int st = j % S;
-                mbar_wait(smem_u32(&bars->kv_empty[st]), ((j / S) & 1) ^ 1);
-                const uint32_t full = map_to_rank(smem_u32(&bars->kv_full[st]), 0);
-                if (leader) mbar_arrive_expect_tx(smem_u32(&bars->kv_full[st]), 2 * (C::kKBytes + C::kVBytes));
-                tma_load_3d_pair(sK + st * C::kKBytes, &tm_k, full, 0, j * kBN + 32 * static_cast<int>(rank), unit);
-                tma_load_3d_pair(sV + st * C::kVBytes, &tm_v, full, 64 * static_cast<int>(rank), j * kBN, unit);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 17 && leader) {
-        // ------------------------------------------------------------ MMA issuer (leader only)
-        constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, 256, kBN);
-        constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, 256, D);
-        constexpr uint32_t idesc_bias = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 0, 256, kBN);
-        const uint64_t dq0 = make_smem_desc(sQ, 16, 8 * D, kSwizzle128B);
-        const uint64_t dk0 = make_smem_desc(sK, 16, 8 * D, kSwizzle128B);
-        const uint64_t dv0 = make_smem_desc(sV, C::kVBytes, 1024, kSwizzle128B);
-        const uint64_t d_bias_a = make_smem_desc(smem_u32(smem + C::kOffBiasA), 128, 256, kSwizzleNone);
-        const uint64_t d_bias_b = make_smem_desc(smem_u32(smem + C::kOffBiasB), 128, 256, kSwizzleNone);
-        mbar_wait(smem_u32(&bars->q_full), 0);
-        auto issue_qk = [&](int x, int j) {
-            const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
-            const uint64_t dk = dk0 + static_cast<uint64_t>(((j % S) * C::kKBytes) >> 4);
-            const uint32_t t_s = tbase + x * 128 + (j & 1) * 64;
-            if (elect_one()) {
-                umma_f16_ss_pair(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
-#pragma unroll
-                for (int kk = 0; kk < D / 32; ++kk)
-                    umma_i8_ss_pair(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2),
-                                    idesc_qk, 1u);
-                umma_commit_pair(smem_u32(&bars->s_full[x][j & 1]));
-            }
-            __syncwarp();
-        };
-        auto wait_kv = [&](int j) {
-            mbar_wait(smem_u32(&bars->kv_full[j % S]), (j / S) & 1);
-            tc_fence_after();
-        };
-        for (int j = 0; j < 2 && j < nkv; ++j) {
-            wait_kv(j);
-            if (j < nkv_a) issue_qk(0, j);
-            if (j < nkv_b) issue_qk(1, j);
-        }
-        for (int j = 0; j < nkv; ++j) {
-            const int st = j % S;
-            const bool next = j + 2 < nkv;
-            if (next) wait_kv(j + 2);
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-                const int nkv_x = x == 0 ? nkv_a : nkv_b;
-                if (j < nkv_x) {
-                    mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
-                    tc_fence_after();
-                    const uint64_t dv = dv0 + static_cast<uint64_t>((st * C::kVBytes) >> 4);
-                    const uint32_t t_p = tbase + x * 128 + (j & 1) * 64;
-                    const uint32_t t_o = tbase + 256 + x * D;
-                    if (elect_one()) {
-#pragma unroll
-                        for (int kk = 0; kk < kBN / 16; ++kk)
-                            umma_f16_ts_pair(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
-                                             (j > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit_pair(smem_u32(&bars->pv_done[x]));
-                        if (j == nkv_x - 1) umma_commit_pair(smem_u32(&bars->o_final[x]));
-                    }
-                    __syncwarp();
-                }
-                if (next && j + 2 < nkv_x) issue_qk(x, j + 2);
-            }
-            if (elect_one()) umma_commit_pair(smem_u32(&bars->kv_empty[st]));
-            __syncwarp();
-        }
-        __syncwarp();
-    } else if (warp < 16) {
-        // ------------------------------------------------------------ softmax (both CTAs)
-        const int x = warp / 8;
-        const int qt = qt0 + x;
-        const int nkv_x = x == 0 ? nkv_a : nkv_b;
-        const int lane_base = (warp % 4) * 32 + ((warp % 8) / 4) * 16;
-        const int half = lane / 16;
-        const int row = lane_base + (lane % 16);
-        const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
-        const uint32_t t_o = tbase + lane_off + 256 + x * D;
-        const int qi = qt * kBM + row;
-        float m = -INFINITY, l = 0.0f;
-        const float qsl = (qt < ntq ? p.qscales[static_cast<size_t>(unit) * ntq + qt] : 1.0f) * kLog2e;
-        const float* ksc = p.kscales + static_cast<size_t>(unit) * ntk;
-        const uint32_t p_full0 = map_to_rank(smem_u32(&bars->p_full[x][0]), 0);
-        const uint32_t p_full1 = map_to_rank(smem_u32(&bars->p_full[x][1]), 0);
-        float ks_next = __ldg(ksc);
-        uint32_t r[32];
-        mbar_wait(smem_u32(&bars->s_full[x][0]), 0);
-        tc_fence_after();
-        tmem_ld16x2_32(tbase + lane_off + x * 128, r);
-        for (int j = 0; j < nkv_x; ++j) {
-            const float ks_cur = ks_next;
-            if (j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
-            const int b = j & 1;
-            tmem_wait_ld_dep(r);
-            const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
-            const int kb = j * kBN;
-            const float cg = qsl * ks_cur;
-            const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
-            bool rescale;
-            float alpha;
-            if (need_mask)
-                alpha = softmax_half<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, nullptr);
-            else
-                alpha = softmax_half<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, nullptr);
-            if (rescale && j > 0) {
-                mbar_wait(smem_u32(&bars->pv_done[x]), (j - 1) & 1);
-                tc_fence_after();
-#pragma unroll 1
-                for (int c = 0; c < D / 2; c += 32) {
-                    uint32_t o[32];
-                    tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tmem_st16x2_32o<D / 2>(t_o + c, o);
-                }
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(b ? p_full1 : p_full0);  // the leader's barrier
-            if (j + 1 < nkv_x) {
-                mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((j + 1) >> 1) & 1);
-                tc_fence_after();
-                tmem_ld16x2_32(tbase + lane_off + x * 128 + (b ^ 1) * 64, r);
-            }
-        }
-        mbar_wait(smem_u32(&bars->o_final[x]), 0);
-        tc_fence_after();
-        l += __shfl_xor_sync(0xffffffffu, l, 16);
-        const float inv_l = 1.0f / l;
-        bool finite = true;
-#pragma unroll 1
-        for (int c = 0; c < D / 2; c += 32) {
-            uint32_t o[32];
-            tmem_ld16x2_32o<D / 2>(t_o + c, o);
-            tmem_wait_ld();
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                finite &= isfinite(__uint_as_float(o[e]));
-                v[e] = __uint_as_float(o[e]) * inv_l;
-            }
-            if (qi < n) {
-                const size_t off = (static_cast<size_t>(unit) * n + qi) * D + half * (D / 2) + c;
-                if (OUT_F32) {
-                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                } else {
-                    uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
-                                            pack_half2(v[8 * e + 4], v[8 * e + 5]), pack_half2(v[8 * e + 6], v[8 * e + 7]));
-                }
-            }
-        }
-        if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync_all();  // the leader's MMAs read the peer's SMEM / TMEM until o_final
-    if (warp == 16) {
-        tc_fence_after();
-        tmem_dealloc_pair<512>(tbase);
-    }
-}
-
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1006,53 +726,8 @@ cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
 }
 
 // The INT32 S dump does not read the scales, so it only needs the per-block build.
-template <bool CAUSAL, bool OUT_F32>
-cudaError_t launch_pair(const AttnParams& p, cudaStream_t s) {
-    using C = CfgPair;
-    CUtensorMap tq, tk, tv;
-    if (!make_map(&tq, p.qcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 128, p.n, p.units, 128, kBM,
-                  CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, 128, p.n, p.units, 128, 32,
-                  CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, 128, p.n, p.units, 64, kBN,
-                  CU_TENSOR_MAP_SWIZZLE_128B))
-        return cudaErrorInvalidValue;
-    AttnParams pp = p;
-    pp.group_units = raster_group_units(p, 128);
-    auto kern = k2_pair<CAUSAL, OUT_F32>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    const int ntq = (p.n + kBM - 1) / kBM;
-    const unsigned clusters = static_cast<unsigned>((ntq + 3) / 4) * static_cast<unsigned>(p.units);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::kSmemBytes;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, pp);
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
-}
-
-#ifndef SAB_K2_PAIR
-#define SAB_K2_PAIR 0
-#endif
-
 template <bool DUMP>
 cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
-    if (SAB_K2_PAIR && !DUMP && !p.per_token && p.d == 128) {
-        const bool c = p.causal != 0, f = p.out_f32 != 0;
-        if (c) return f ? launch_pair<true, true>(p, s) : launch_pair<true, false>(p, s);
-        return f ? launch_pair<false, true>(p, s) : launch_pair<false, false>(p, s);
-    }
     if (!DUMP && p.per_token) return dispatch_pt<false, true>(p, s);
     return dispatch_pt<DUMP, false>(p, s);
 }
