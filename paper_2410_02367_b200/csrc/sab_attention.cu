@@ -149,7 +149,6 @@ struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
     uint64_t q_full;
     uint64_t kv_full[16], kv_empty[16];
     uint64_t s_full[2][2], p_full[2][2], pv_done[2], o_final[2];
-    uint64_t q_empty, o_free[2];  // persistent kernel: Q^ buffer and O_x reusable
     uint32_t tmem_base;
 };
 
@@ -643,316 +642,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// ==================================================================== persistent K2
-// k2_attention's pipeline run by one resident CTA per SM over a static list of work
-// items (unit, query-tile pair) in the same L2-aware raster order, CTA b taking items
-// b, b + grid, ...  Across items the barrier phases continue (global step counters per
-// query tile), the producer prefetches the next item's Q^ as soon as the current item's
-// last QK^T is issued (q_empty) and its K^/V tiles as ring stages free up, and the MMA
-// issuer starts the next item's QK^T while the softmax warps still run the previous
-// epilogue -- only the first P V of a tile waits for its O to be read out (o_free).
-struct Item {
-    int unit, qt0, nkv_a, nkv_b;
-    bool has_b;
-};
-
-template <bool CAUSAL>
-__device__ __forceinline__ Item item_of(const AttnParams& p, int it, int ntq, int ntk, int npair) {
-    Item w;
-    const int gu = p.group_units;
-    const int g = it / (gu * npair);
-    const int r = it - g * gu * npair;
-    const int gsz = min(gu, p.units - g * gu);
-    w.unit = g * gu + r % gsz;
-    const int pair = npair - 1 - r / gsz;
-    w.qt0 = 2 * pair;
-    w.has_b = w.qt0 + 1 < ntq;
-    w.nkv_a = CAUSAL ? min(2 * w.qt0 + 2, ntk) : ntk;
-    w.nkv_b = w.has_b ? (CAUSAL ? min(2 * w.qt0 + 4, ntk) : ntk) : 0;
-    return w;
-}
-
-template <int D, bool CAUSAL, bool OUT_F32>
-__global__ void __launch_bounds__(kThreads, 1)
-    k2_persist(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
-    using C = Cfg<D>;
-    constexpr int S = C::kStages;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
-    const uint32_t sQ = smem_u32(smem + C::kOffQ);
-    const uint32_t sK = smem_u32(smem + C::kOffK);
-    const uint32_t sV = smem_u32(smem + C::kOffV);
-    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x / 32), 0);
-    const int lane = threadIdx.x % 32;
-    const int n = p.n;
-    const int ntq = (n + kBM - 1) / kBM;
-    const int ntk = (n + kBN - 1) / kBN;
-    const int npair = (ntq + 1) / 2;
-    const int n_items = npair * p.units;
-
-    {
-        uint4* bias = reinterpret_cast<uint4*>(smem + C::kOffBiasA);
-        const uint4 a2048 = make_uint4(0x68006800u, 0x68006800u, 0x68006800u, 0x68006800u);
-        const uint4 b384 = make_uint4(0x5E005E00u, 0x5E005E00u, 0x5E005E00u, 0x5E005E00u);
-        for (int i = threadIdx.x; i < (8192 + 4096) / 16; i += kThreads) bias[i] = i < 8192 / 16 ? a2048 : b384;
-        fence_proxy_async_smem();
-    }
-    if (threadIdx.x == 0) {
-        mbar_init(smem_u32(&bars->q_full), 1);
-        mbar_init(smem_u32(&bars->q_empty), 1);
-        for (int s2 = 0; s2 < S; ++s2) {
-            mbar_init(smem_u32(&bars->kv_full[s2]), 1);
-            mbar_init(smem_u32(&bars->kv_empty[s2]), 1);
-        }
-        for (int x = 0; x < 2; ++x) {
-            for (int b = 0; b < 2; ++b) {
-                mbar_init(smem_u32(&bars->s_full[x][b]), 1);
-                mbar_init(smem_u32(&bars->p_full[x][b]), 8);
-            }
-            mbar_init(smem_u32(&bars->pv_done[x]), 1);
-            mbar_init(smem_u32(&bars->o_final[x]), 1);
-            mbar_init(smem_u32(&bars->o_free[x]), 8);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 16) tmem_alloc<512>(smem_u32(&bars->tmem_base));
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tbase = bars->tmem_base;
-
-    if (warp == 16) {
-        // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            tma_prefetch_desc(&tm_q);
-            tma_prefetch_desc(&tm_k);
-            tma_prefetch_desc(&tm_v);
-            int kvi = 0, ic = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
-                const Item w = item_of<CAUSAL>(p, it, ntq, ntk, npair);
-                const int nkv = max(w.nkv_a, w.nkv_b);
-                if (ic > 0) mbar_wait(smem_u32(&bars->q_empty), (ic - 1) & 1);
-                mbar_arrive_expect_tx(smem_u32(&bars->q_full), (w.has_b ? 2 : 1) * C::kQBytes);
-                tma_load_3d(sQ, &tm_q, smem_u32(&bars->q_full), 0, w.qt0 * kBM, w.unit);
-                if (w.has_b) tma_load_3d(sQ + C::kQBytes, &tm_q, smem_u32(&bars->q_full), 0, (w.qt0 + 1) * kBM, w.unit);
-                for (int j = 0; j < nkv; ++j, ++kvi) {
-                    const int st = kvi % S;
-                    mbar_wait(smem_u32(&bars->kv_empty[st]), ((kvi / S) & 1) ^ 1);
-                    const uint32_t full = smem_u32(&bars->kv_full[st]);
-                    mbar_arrive_expect_tx(full, C::kKBytes + C::kVBytes);
-                    tma_load_3d(sK + st * C::kKBytes, &tm_k, full, 0, j * kBN, w.unit);
-#pragma unroll
-                    for (int c = 0; c < D / 64; ++c)
-                        tma_load_3d(sV + st * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, j * kBN, w.unit);
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp == 17) {
-        // ------------------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, kBN);
-        constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
-        constexpr uint32_t idesc_bias = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 0, kBM, kBN);
-        const uint64_t dq0 = make_smem_desc(sQ, 16, C::kSboQK, C::kSwizzleQK);
-        const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
-        const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
-        const uint64_t d_bias_a = make_smem_desc(smem_u32(smem + C::kOffBiasA), 128, 256, kSwizzleNone);
-        const uint64_t d_bias_b = make_smem_desc(smem_u32(smem + C::kOffBiasB), 128, 256, kSwizzleNone);
-        int kvi = 0, ic = 0;
-        int gs[2] = {0, 0}, oc[2] = {0, 0};  // per tile: global KV-step count, items with work
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
-            const Item w = item_of<CAUSAL>(p, it, ntq, ntk, npair);
-            const int nkv = max(w.nkv_a, w.nkv_b);
-            // QK_x(j) (item-local j) into S_x[(gs[x] + j) % 2].
-            auto issue_qk = [&](int x, int j) {
-                const int st = (kvi + j) % S;
-                const int gj = gs[x] + j;
-                const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
-                const uint64_t dk = dk0 + static_cast<uint64_t>((st * C::kKBytes) >> 4);
-                const uint32_t t_s = tbase + x * 128 + (gj & 1) * 64;
-                if (elect_one()) {
-                    umma_f16_ss(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
-#pragma unroll
-                    for (int kk = 0; kk < D / 32; ++kk)
-                        umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2),
-                                   idesc_qk, 1u);
-                    umma_commit(smem_u32(&bars->s_full[x][gj & 1]));
-                }
-                __syncwarp();
-            };
-            auto wait_kv = [&](int j) {
-                mbar_wait(smem_u32(&bars->kv_full[(kvi + j) % S]), ((kvi + j) / S) & 1);
-                tc_fence_after();
-            };
-            auto release_q = [&]() {  // every QK^T of this item issued: Q^ free once they finish
-                if (elect_one()) umma_commit(smem_u32(&bars->q_empty));
-                __syncwarp();
-            };
-            mbar_wait(smem_u32(&bars->q_full), ic & 1);
-            tc_fence_after();
-            for (int j = 0; j < 2 && j < nkv; ++j) {
-                wait_kv(j);
-                if (j < w.nkv_a) issue_qk(0, j);
-                if (j < w.nkv_b) issue_qk(1, j);
-            }
-            if (nkv <= 2) release_q();
-            for (int j = 0; j < nkv; ++j) {
-                const bool next = j + 2 < nkv;
-                if (next) wait_kv(j + 2);
-#pragma unroll
-                for (int x = 0; x < 2; ++x) {
-                    const int nkv_x = x == 0 ? w.nkv_a : w.nkv_b;
-                    if (j < nkv_x) {
-                        const int gj = gs[x] + j;
-                        if (j == 0 && oc[x] > 0) mbar_wait(smem_u32(&bars->o_free[x]), (oc[x] - 1) & 1);
-                        mbar_wait(smem_u32(&bars->p_full[x][gj & 1]), (gj >> 1) & 1);
-                        tc_fence_after();
-                        const uint64_t dv = dv0 + static_cast<uint64_t>((((kvi + j) % S) * C::kVBytes) >> 4);
-                        const uint32_t t_p = tbase + x * 128 + (gj & 1) * 64;
-                        const uint32_t t_o = tbase + 256 + x * D;
-                        if (elect_one()) {
-#pragma unroll
-                            for (int kk = 0; kk < kBN / 16; ++kk)
-                                umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
-                                            (j > 0 || kk > 0) ? 1u : 0u);
-                            umma_commit(smem_u32(&bars->pv_done[x]));
-                            if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
-                        }
-                        __syncwarp();
-                    }
-                    if (next && j + 2 < nkv_x) issue_qk(x, j + 2);
-                }
-                if (j + 3 == nkv) release_q();  // QK(nkv - 1) went out in this iteration
-                if (elect_one()) umma_commit(smem_u32(&bars->kv_empty[(kvi + j) % S]));
-                __syncwarp();
-            }
-            kvi += nkv;
-            for (int x = 0; x < 2; ++x) {
-                const int nkv_x = x == 0 ? w.nkv_a : w.nkv_b;
-                if (nkv_x > 0) {
-                    gs[x] += nkv_x;
-                    ++oc[x];
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp < 16) {
-        // ------------------------------------------------------------ softmax warpgroups
-        const int x = warp / 8;
-        const int lane_base = (warp % 4) * 32 + ((warp % 8) / 4) * 16;
-        const int half = lane / 16;
-        const int row = lane_base + (lane % 16);
-        const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
-        const uint32_t t_o = tbase + lane_off + 256 + x * D;
-        int gs = 0, oc = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const Item w = item_of<CAUSAL>(p, it, ntq, ntk, npair);
-            const int nkv_x = x == 0 ? w.nkv_a : w.nkv_b;
-            if (nkv_x == 0) continue;
-            const int unit = w.unit;
-            const int qt = w.qt0 + x;
-            const int qi = qt * kBM + row;
-            float m = -INFINITY, l = 0.0f;
-            const float qsl = p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
-            const float* ksc = p.kscales + static_cast<size_t>(unit) * ntk;
-            float ks_next = __ldg(ksc);
-            uint32_t r[32];
-            mbar_wait(smem_u32(&bars->s_full[x][gs & 1]), (gs >> 1) & 1);
-            tc_fence_after();
-            tmem_ld16x2_32(tbase + lane_off + x * 128 + (gs & 1) * 64, r);
-            for (int j = 0; j < nkv_x; ++j) {
-                const int gj = gs + j;
-                const float ks_cur = ks_next;
-                if (j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
-                const int b = gj & 1;
-                tmem_wait_ld_dep(r);
-                const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
-                const int kb = j * kBN;
-                const float cg = qsl * ks_cur;
-                const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
-                bool rescale;
-                float alpha;
-                if (need_mask)
-                    alpha = softmax_half<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, nullptr);
-                else
-                    alpha = softmax_half<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, nullptr);
-                if (rescale && j > 0) {
-                    mbar_wait(smem_u32(&bars->pv_done[x]), (gj - 1) & 1);
-                    tc_fence_after();
-#pragma unroll 1
-                    for (int c = 0; c < D / 2; c += 32) {
-                        uint32_t o[32];
-                        tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                        tmem_st16x2_32o<D / 2>(t_o + c, o);
-                    }
-                }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));
-                if (j + 1 < nkv_x) {
-                    mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((gj + 1) >> 1) & 1);
-                    tc_fence_after();
-                    tmem_ld16x2_32(tbase + lane_off + x * 128 + (b ^ 1) * 64, r);
-                }
-            }
-            // -------------------------------------------------------- epilogue
-            mbar_wait(smem_u32(&bars->o_final[x]), oc & 1);
-            tc_fence_after();
-            l += __shfl_xor_sync(0xffffffffu, l, 16);
-            const float inv_l = 1.0f / l;
-            bool finite = true;
-#pragma unroll 1
-            for (int c = 0; c < D / 2; c += 32) {
-                uint32_t o[32];
-                tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                tmem_wait_ld();
-                if (c + 32 >= D / 2) {  // O_x fully read: the next item's first P V may overwrite it
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&bars->o_free[x]));
-                }
-                float v[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    finite &= isfinite(__uint_as_float(o[e]));
-                    v[e] = __uint_as_float(o[e]) * inv_l;
-                }
-                if (qi < n) {
-                    const size_t off = (static_cast<size_t>(unit) * n + qi) * D + half * (D / 2) + c;
-                    if (OUT_F32) {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                    } else {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
-                                                pack_half2(v[8 * e + 4], v[8 * e + 5]), pack_half2(v[8 * e + 6], v[8 * e + 7]));
-                    }
-                }
-            }
-            if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
-            gs += nkv_x;
-            ++oc;
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 16) {
-        tc_fence_after();
-        tmem_dealloc<512>(tbase);
-    }
-}
-
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1037,51 +726,8 @@ cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
 }
 
 // The INT32 S dump does not read the scales, so it only needs the per-block build.
-int sm_count_attn() {
-    static const int n = [] {
-        int dev = 0, v = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
-}
-
-template <int D, bool CAUSAL, bool OUT_F32>
-cudaError_t launch_persist(const AttnParams& p, cudaStream_t s) {
-    using C = Cfg<D>;
-    CUtensorMap tq, tk, tv;
-    const CUtensorMapSwizzle swqk = D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    if (!make_map(&tq, p.qcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBM, swqk) ||
-        !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBN, swqk) ||
-        !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, kBN, CU_TENSOR_MAP_SWIZZLE_128B))
-        return cudaErrorInvalidValue;
-    AttnParams pp = p;
-    pp.group_units = raster_group_units(p, D);
-    auto kern = k2_persist<D, CAUSAL, OUT_F32>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    const int ntq = (p.n + kBM - 1) / kBM;
-    const int items = ((ntq + 1) / 2) * p.units;
-    const unsigned grid = static_cast<unsigned>(std::min(items, sm_count_attn()));
-    kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, pp);
-    return cudaGetLastError();
-}
-
-#ifndef SAB_K2_PERSIST
-#define SAB_K2_PERSIST 0
-#endif
-
 template <bool DUMP>
 cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
-    if (SAB_K2_PERSIST && !DUMP && !p.per_token) {
-        const bool c = p.causal != 0, f = p.out_f32 != 0;
-        if (p.d == 128)
-            return c ? (f ? launch_persist<128, true, true>(p, s) : launch_persist<128, true, false>(p, s))
-                     : (f ? launch_persist<128, false, true>(p, s) : launch_persist<128, false, false>(p, s));
-        if (p.d == 64)
-            return c ? (f ? launch_persist<64, true, true>(p, s) : launch_persist<64, true, false>(p, s))
-                     : (f ? launch_persist<64, false, true>(p, s) : launch_persist<64, false, false>(p, s));
-    }
     if (!DUMP && p.per_token) return dispatch_pt<false, true>(p, s);
     return dispatch_pt<DUMP, false>(p, s);
 }
