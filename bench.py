@@ -386,6 +386,15 @@ def main():
                         "ms_per_step": k1_mean_ms, "alg_bytes": k1_alg, "min_dram_bytes_with_k_reread": k1_bytes},
         "clocks": sampler.summary(),
     }
+    # Second bound of K2: one exp2 per attended (query, key) pair on MUFU (16 lanes/clk/SM,
+    # profiles/r01_micro_mufu.txt); 2 of every 16 run on the FMA pipe instead.
+    clk = line["clocks"].get("sm_mhz") or 1965
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    exps = shard_ops / (4.0 * d)
+    line["roofline_xu"] = {"bound": "xu (MUFU ex2)", "achieved": exps / (k2_mean_ms * 1e-3) / 1e12,
+                           "peak": 16.0 * sms * clk * 1e6 / 1e12, "unit": "Texp/s",
+                           "frac": exps / (k2_mean_ms * 1e-3) / (16.0 * sms * clk * 1e6),
+                           "note": "algorithmic exponentials (one per attended pair); 2/16 run on the FMA pipe"}
     if world == 1 and not args.no_cpu_baseline and not per_token:
         threads = args.cpu_threads or os.cpu_count() or 1
         v_cpu, s_cpu, sdesc, used, kind = cpu_reference_sample(wl, threads)

@@ -80,10 +80,16 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
 constexpr int kMaskedAcc = 0;              // sentinel below any biased S value (bits of +0.0f)
-#ifndef SAB_POLY_PER16
-#define SAB_POLY_PER16 2
+// Exponentials (of every 16) evaluated by exp2_poly2 on the FMA pipe instead of MUFU,
+// per head dim (d=64 is MUFU-bound, d=128 closer to the tensor/SMEM bound).
+#ifndef SAB_POLY128
+#define SAB_POLY128 2
 #endif
-constexpr int kPolyPer16 = SAB_POLY_PER16;  // exponentials (of 16) evaluated by exp2_poly2 on the FMA pipe
+#ifndef SAB_POLY64
+#define SAB_POLY64 2
+#endif
+template <int D>
+constexpr int poly_per16() { return D == 64 ? SAB_POLY64 : SAB_POLY128; }
 constexpr float kMagicF = 12582912.0f;     // 2^23 + 2^22
 
 // ------------------------------------------------------------ packed fp32 math
@@ -191,7 +197,7 @@ __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
 // the running max m (log2 units) and this thread's partial row sum l; returns the
 // O rescale factor (1 when the warp skips the lazy rescale).  `dump` receives
 // the raw half row.
-template <bool MASK, bool CAUSAL>
+template <bool MASK, bool CAUSAL, int POLY>
 __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t ts, int half, float cg, int kb, int qi,
                                               int n, float& m, float& l, bool& rescale, int32_t* dump,
                                               int trole = -1, int ttile = 0) {
@@ -234,7 +240,7 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
         const int c = 2 * i;
         const f2 t = ffma2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, cg2, bg);
         f2 pp;
-        if ((c & 15) >= 16 - kPolyPer16) {  // part of the exponentials on the FMA pipe
+        if ((c & 15) >= 16 - POLY) {  // part of the exponentials on the FMA pipe
             pp = exp2_poly2(t);
         } else {
             pp = f2{ex2(t.x), ex2(t.y)};
@@ -259,7 +265,7 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
 // dkp points at this thread's 32 key scales (K1 pads each unit's scale row to a
 // multiple of 64, so the float4 loads stay in bounds); r is overwritten with the
 // scores.  Same contract as softmax_half otherwise.
-template <bool MASK, bool CAUSAL>
+template <bool MASK, bool CAUSAL, int POLY>
 __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts, int half, float dq, const float* dkp,
                                                  int kb, int qi, int n, float& m, float& l, bool& rescale,
                                                  int32_t* dump) {
@@ -309,7 +315,7 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
         const int c = 2 * i;
         const f2 t = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-mref, -mref});
         f2 pp;
-        if ((c & 15) >= 16 - kPolyPer16) {
+        if ((c & 15) >= 16 - POLY) {
             pp = exp2_poly2(t);
         } else {
             pp = f2{ex2(t.x), ex2(t.y)};
@@ -555,13 +561,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (PT) {
                     const float* dkp = ksc + kb + 32 * half;
                     if (need_mask)
-                        alpha = softmax_half_pt<true, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
+                        alpha = softmax_half_pt<true, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
                     else
-                        alpha = softmax_half_pt<false, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
+                        alpha = softmax_half_pt<false, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
                 } else if (need_mask) {
-                    alpha = softmax_half<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
+                    alpha = softmax_half<true, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
                 } else {
-                    alpha = softmax_half<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
+                    alpha = softmax_half<false, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
                 }
                 if (tr) SAB_STAMP(x, j, 2);
                 if (rescale && j > 0) {
