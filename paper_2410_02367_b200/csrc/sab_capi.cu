@@ -123,8 +123,14 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// K1's grid.y carries the unit index: one device call covers at most 65535 units (the
+// host-buffer path splits larger shards into chunks).
+constexpr int64_t kMaxUnitsPerLaunch = 65535;
+
 int enqueue_prepass(const sab_desc* d, const sab_ws_layout& L, const void* q, const void* k, const void* v, void* ws,
                     cudaStream_t s, bool reset) {
+    if (units_of(d) > kMaxUnitsPerLaunch)
+        return set_error(SAB_ERR_UNSUPPORTED, "sab_prepass: batch*heads above 65535 per device call");
     if (reset) {
         cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t) * (1 + size_t(units_of(d))), s);
         if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: status reset");
@@ -420,7 +426,8 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     const size_t unit_in_bytes = 3 * unit_elems * in_e;
     const size_t by_bytes = std::max<size_t>(1, (24u << 20) / unit_in_bytes);
     const size_t by_count = std::max<size_t>(1, size_t(job->count) / 8);
-    const int chunk = int(std::max<size_t>(1, std::min<size_t>(job->count, std::min(by_bytes, by_count))));
+    const int chunk = int(std::max<size_t>(
+        1, std::min<size_t>(std::min<size_t>(job->count, size_t(kMaxUnitsPerLaunch)), std::min(by_bytes, by_count))));
     const int n_chunks = (job->count + chunk - 1) / chunk;
 
     sab_desc cd = *D;

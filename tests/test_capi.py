@@ -36,6 +36,7 @@ def test_desc_validation_mirrors_reference():
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=_lib.SAB_PV_FP16_TILE))) == \
         _lib.SAB_ERR_UNSUPPORTED
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, per_token=True))) == _lib.SAB_OK
+    assert lib.sab_check_desc(C.byref(_lib.desc(2, 32768, 64, 64))) == _lib.SAB_OK  # host path chunks it
     bad_g = _lib.desc(1, 1, 1024, 64)
     bad_g.qk_granularity = 2  # per-tensor is not a SAGEAttn variant
     assert lib.sab_check_desc(C.byref(bad_g)) == _lib.SAB_ERR_UNSUPPORTED

@@ -230,3 +230,21 @@ def test_against_reference_fixtures(cuda, path):
     o, ref = o.reshape(-1, n, d), g["o_fp32acc"].reshape(-1, n, d)
     cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
     assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)
+
+
+def test_many_units_host_path_and_device_limit(cuda, oracle):
+    """B*H above K1's 65535-unit grid: the host path chunks it, a single device call refuses it."""
+    import torch
+
+    from paper_2410_02367_b200 import attention_fwd_host, sage_attention_cuda
+
+    b, h, n, d = 1, 70000, 3, 64
+    q, k, v = (x.astype(np.float16) for x in _qkv(b, h, n, d))
+    o = attention_fwd_host(q, k, v, False, np.empty(q.shape, np.float32), devices=[0]).reshape(-1, n, d)
+    sel = np.array([0, 65534, 65535, 69999])
+    ref, _ = oracle.sage_b(q.reshape(-1, n, d)[sel].astype(np.float32), k.reshape(-1, n, d)[sel].astype(np.float32),
+                           v.reshape(-1, n, d)[sel].astype(np.float32), False, pv_fp32=True)
+    assert cosine_sim(o[sel], ref) >= COS_MIN and relative_l1(o[sel], ref) <= REL_L1_MAX
+    qd, kd, vd = _to_dev([q, k, v], torch.float16, cuda)
+    with pytest.raises(ValueError, match="65535"):
+        sage_attention_cuda(qd, kd, vd)
