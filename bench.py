@@ -63,12 +63,15 @@ def paper_ops(units: int, n: int, d: int, causal: bool) -> float:
 
 
 def measured_peaks():
+    """MEASURED_PEAKS.json (driver-written) or the profiling guide's fallback, key by key."""
+    fallback = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p, "measured"
-    except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+    except (OSError, ValueError):
+        return fallback, "fallback"
+    out = {k: float(p[k]) if isinstance(p.get(k), (int, float)) else v for k, v in fallback.items()}
+    return out, "measured" if all(isinstance(p.get(k), (int, float)) for k in fallback) else "measured/fallback"
 
 
 class ClockSampler:
