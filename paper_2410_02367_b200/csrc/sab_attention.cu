@@ -78,6 +78,7 @@ constexpr int kBN = 64;    // keys per KV tile = one K scale group
 constexpr int kThreads = 576;  // 16 softmax warps + TMA producer + MMA issuer
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr float kRescaleLimit = 256.0f;    // 2^kRescaleThreshold
 constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
 constexpr int kMaskedAcc = 0;              // sentinel below any biased S value (bits of +0.0f)
 // Exponentials (of every 16) evaluated by exp2_poly2 on the FMA pipe instead of MUFU,
@@ -268,7 +269,7 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
 template <bool MASK, bool CAUSAL, int POLY>
 __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts, int half, float dq, const float* dkp,
                                                  int kb, int qi, int n, float& m, float& l, bool& rescale,
-                                                 int32_t* dump) {
+                                                 int32_t* dump, bool first) {
     const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
     if (dump) {
 #pragma unroll
@@ -277,6 +278,47 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
                                                            r[c + 3] - kMagicI);
     }
     const int lim2 = MASK ? opaque(lim) : lim;
+    if (!first) {
+        // Lazy rescaling keeps m until a row max exceeds it by 2^8, so after the first tile
+        // the exponentials run in one pass against the current m, and the exact two-pass
+        // path below is taken only if some p of the warp exceeds 2^8.
+        f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+        float pm[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[16];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const float4 dk4 = __ldg(reinterpret_cast<const float4*>(dkp) + g);
+            const f2 w0 = ffma2(f2{dq, dq}, f2{dk4.x, dk4.y}, f2{0.0f, 0.0f});
+            const f2 w1 = ffma2(f2{dq, dq}, f2{dk4.z, dk4.w}, f2{0.0f, 0.0f});
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+                const int c = 4 * g + e;
+                const f2 a = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-kMagicF, -kMagicF});
+                const f2 t = ffma2(a, e == 0 ? w0 : w1, f2{-m, -m});
+                f2 pp;
+                if ((c & 15) >= 16 - POLY) {
+                    pp = exp2_poly2(t);
+                } else {
+                    pp = f2{ex2(t.x), ex2(t.y)};
+                }
+                if (MASK) {
+                    pp.x = (c >= lim2) ? 0.0f : pp.x;
+                    pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+                }
+                pk[c / 2] = pack_half2(pp.x, pp.y);
+                acc[g & 3] = fadd2(acc[g & 3], pp);
+                pm[g & 3] = fmaxf(pm[g & 3], fmaxf(pp.x, pp.y));
+            }
+        }
+        const float pmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
+        if (!__any_sync(0xffffffffu, pmax > kRescaleLimit)) {
+            tmem_st16x2_16(ts, pk);
+            const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+            l += sum.x + sum.y;
+            rescale = false;
+            return 1.0f;
+        }
+    }
     float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
@@ -561,9 +603,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (PT) {
                     const float* dkp = ksc + kb + 32 * half;
                     if (need_mask)
-                        alpha = softmax_half_pt<true, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
+                        alpha = softmax_half_pt<true, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump,
+                                                                       j == 0);
                     else
-                        alpha = softmax_half_pt<false, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump);
+                        alpha = softmax_half_pt<false, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale,
+                                                                        dump, j == 0);
                 } else if (need_mask) {
                     alpha = softmax_half<true, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
                 } else {
