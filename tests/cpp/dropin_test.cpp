@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
+#include <string>
 #include <iostream>
 
 static void read_into(const char* path, sageattn::Tensor4f& t) {
@@ -47,6 +48,10 @@ int main(int argc, char** argv) {
     const sageattn::Tensor4f out = sageattn::sage_attention(in, sageattn::SageVariant::B, opts);
     std::ofstream(argv[9], std::ios::binary)
         .write(reinterpret_cast<const char*>(out.data.data()), std::streamsize(out.size() * sizeof(float)));
+    // SAGEAttn-T through the same entry point (per-token Q/K scales).
+    const sageattn::Tensor4f out_t = sageattn::sage_attention(in, sageattn::SageVariant::T);
+    std::ofstream(std::string(argv[9]) + ".t", std::ios::binary)
+        .write(reinterpret_cast<const char*>(out_t.data.data()), std::streamsize(out_t.size() * sizeof(float)));
     std::printf("MACS %llu %llu\n", (unsigned long long)diag.s_stage_macs, (unsigned long long)diag.pv_stage_macs);
 
     bool ok = true;

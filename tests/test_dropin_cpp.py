@@ -1,6 +1,6 @@
 """The C++ drop-in (include/sageattn/attention.hpp): an application written
 against the reference API compiles, links libsageattn_b200.so, and on a B200
-returns the SAGEAttn-B output within tolerance of the reference's FP32-acc arm,
+returns the SAGEAttn-B (and -T) output within tolerance of the reference's FP32-acc arm,
 with the reference's MAC counters and exceptions."""
 import os
 import subprocess
@@ -51,3 +51,6 @@ def test_dropin_runs_on_b200(tmp_path, cuda, oracle, shape, causal):
     assert cosine_sim(o, ref) >= 0.9999 and relative_l1(o, ref) <= 2e-3
     s, p = (int(x) for x in r.stdout.split("MACS")[1].split()[:2])
     assert (s, p) == tuple(int(x) for x in macs)
+    o_t = np.fromfile(str(out) + ".t", np.float32).reshape(b * h, n, d)
+    ref_t, _ = oracle.sage(q, k, v, causal, pv_fp32=True, per_token=True)
+    assert cosine_sim(o_t, ref_t) >= 0.9999 and relative_l1(o_t, ref_t) <= 2e-3
