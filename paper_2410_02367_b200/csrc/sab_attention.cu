@@ -6,6 +6,8 @@
 //   causal tile classes (79-94, 399-427)    -> fully masked KV tiles are never issued; the element
 //                                              mask runs only on the diagonal / ragged tail tile
 //   online softmax (429-443)                -> registers, two threads per query row
+//   per-token scales (variant T, 410-413)   -> per-element dQ[row] * dK[key]; one pass against the
+//                                              stale max, exact two-pass fallback (softmax_half_pt)
 //   P~ V with binary16 operands (447-475)   -> P packed to fp16 into TMEM (aliasing S),
 //                                              tcgen05.mma kind::f16 with A from TMEM, V from SMEM,
 //                                              FP32 accumulator in TMEM (the pv_fp32_accumulator arm)
@@ -135,7 +137,13 @@ __device__ __forceinline__ f2 exp2_poly2(f2 x) {
 
 template <int D>
 struct Cfg {
-    static constexpr int kStages = D == 128 ? 6 : 8;
+#ifndef SAB_STAGES128
+#define SAB_STAGES128 6
+#endif
+#ifndef SAB_STAGES64
+#define SAB_STAGES64 8
+#endif
+    static constexpr int kStages = D == 128 ? SAB_STAGES128 : SAB_STAGES64;  // K^/V ring depth
     static constexpr int kQBytes = kBM * D;
     static constexpr int kKBytes = kBN * D;
     static constexpr int kVBytes = kBN * D * 2;
