@@ -140,10 +140,17 @@ struct Cfg {
 #ifndef SAB_STAGES128
 #define SAB_STAGES128 6
 #endif
+#ifndef SAB_NB64
+#define SAB_NB64 2
+#endif
 #ifndef SAB_STAGES64
 #define SAB_STAGES64 8
 #endif
     static constexpr int kStages = D == 128 ? SAB_STAGES128 : SAB_STAGES64;  // K^/V ring depth
+    // S buffers per query tile: 3 when O is narrow enough (d=64: 2 x 3 x 64 + 2 x 64 = 512
+    // TMEM columns), else 2.  A deeper S ring gives QK_x(j+NB) more slack behind PV_x(j).
+    static constexpr int kNB = D == 64 ? SAB_NB64 : 2;
+    static constexpr int kOffO = 2 * kNB * 64;  // TMEM column of O_A
     static constexpr int kQBytes = kBM * D;
     static constexpr int kKBytes = kBN * D;
     static constexpr int kVBytes = kBN * D * 2;
@@ -163,7 +170,7 @@ struct Cfg {
 struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
     uint64_t q_full;
     uint64_t kv_full[16], kv_empty[16];
-    uint64_t s_full[2][2], p_full[2][2], pv_done[2], o_final[2];
+    uint64_t s_full[2][3], p_full[2][3], pv_done[2][3], o_final[2];
     uint32_t tmem_base;
 };
 
@@ -389,7 +396,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
     using C = Cfg<D>;
     constexpr int S = C::kStages;
+    constexpr int NB = C::kNB;
     static_assert(sizeof(Bars) <= 512, "barrier block overflows its reservation");
+    static_assert(C::kOffO + 2 * D <= 512, "TMEM budget");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars* bars = reinterpret_cast<Bars*>(smem + C::kOffBar);
@@ -444,11 +453,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(smem_u32(&bars->kv_empty[s]), 1);
         }
         for (int x = 0; x < 2; ++x) {
-            for (int b = 0; b < 2; ++b) {
+            for (int b = 0; b < C::kNB; ++b) {
                 mbar_init(smem_u32(&bars->s_full[x][b]), 1);
                 mbar_init(smem_u32(&bars->p_full[x][b]), 8);  // one arrival per softmax warp
+                mbar_init(smem_u32(&bars->pv_done[x][b]), 1);
             }
-            mbar_init(smem_u32(&bars->pv_done[x]), 1);
             mbar_init(smem_u32(&bars->o_final[x]), 1);
         }
         fence_barrier_init();
@@ -504,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = j % S;
             const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
             const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
-            const uint32_t t_s = tbase + x * 128 + (j & 1) * 64;
+            const uint32_t t_s = tbase + x * (NB * 64) + (j % NB) * 64;
             if (elect_one()) {
                 // Bias MMA: S = 2^23 + 2^22 as binary32 (bits 0x4B400000) from constant fp16
                 // operands, then the INT32 QK^T products accumulate onto those bits, so the
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < D / 32; ++kk)
                     umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2), idesc_qk,
                                1u);
-                umma_commit(smem_u32(&bars->s_full[x][j & 1]));
+                umma_commit(smem_u32(&bars->s_full[x][j % NB]));
             }
             __syncwarp();
         };
@@ -524,38 +533,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (lane == 0) SAB_STAMP(2, j, 1);
         };
-        for (int j = 0; j < 2 && j < nkv; ++j) {
+        for (int j = 0; j < NB && j < nkv; ++j) {
             wait_kv(j);
             if (j < nkv_a) issue_qk(0, j);
             if (j < nkv_b) issue_qk(1, j);
         }
         for (int j = 0; j < nkv; ++j) {
             const int s = j % S;
-            const bool next = j + 2 < nkv;
-            if (next) wait_kv(j + 2);
+            const bool next = j + NB < nkv;
+            if (next) wait_kv(j + NB);
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
                 const int nkv_x = x == 0 ? nkv_a : nkv_b;
                 if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
                     if (lane == 0) SAB_STAMP(2 + x, j, 3);
-                    mbar_wait(smem_u32(&bars->p_full[x][j & 1]), (j >> 1) & 1);
+                    mbar_wait(smem_u32(&bars->p_full[x][j % NB]), (j / NB) & 1);
                     tc_fence_after();
                     if (lane == 0) SAB_STAMP(2 + x, j, 4);
                     const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
-                    const uint32_t t_p = tbase + x * 128 + (j & 1) * 64;
-                    const uint32_t t_o = tbase + 256 + x * D;
+                    const uint32_t t_p = tbase + x * (NB * 64) + (j % NB) * 64;
+                    const uint32_t t_o = tbase + C::kOffO + x * D;
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < kBN / 16; ++kk)
                             umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
                                         (j > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit(smem_u32(&bars->pv_done[x]));
+                        umma_commit(smem_u32(&bars->pv_done[x][j % NB]));
                         if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
                     }
                     __syncwarp();
                     if (lane == 0) SAB_STAMP(2 + x, j, 5);
                 }
-                if (next && j + 2 < nkv_x) issue_qk(x, j + 2);
+                if (next && j + NB < nkv_x) issue_qk(x, j + NB);
             }
             if (elect_one()) umma_commit(smem_u32(&bars->kv_empty[s]));  // K^(j), V(j) free once these MMAs finish
             __syncwarp();
@@ -572,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int half = lane / 16;
         const int row = lane_base + (lane % 16);
         const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
-        const uint32_t t_o = tbase + lane_off + 256 + x * D;
+        const uint32_t t_o = tbase + lane_off + C::kOffO + x * D;
         const int qi = qt * kBM + row;
         float m = -INFINITY, l = 0.0f;
         if (nkv_x > 0) {
@@ -591,14 +600,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tr) SAB_STAMP(x, 0, 0);
             mbar_wait(smem_u32(&bars->s_full[x][0]), 0);
             tc_fence_after();
-            tmem_ld16x2_32(tbase + lane_off + x * 128, r);
+            tmem_ld16x2_32(tbase + lane_off + x * (NB * 64), r);
             for (int j = 0; j < nkv_x; ++j) {
                 const float ks_cur = ks_next;
                 if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
-                const int b = j & 1;
+                const int b = j % NB;
                 tmem_wait_ld_dep(r);
                 if (tr) SAB_STAMP(x, j, 1);
-                const uint32_t t_s = tbase + lane_off + x * 128 + b * 64;
+                const uint32_t t_s = tbase + lane_off + x * (NB * 64) + b * 64;
                 int32_t* dump = (DUMP && qt == p.dump_qtile)
                                     ? p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN + 32 * half
                                     : nullptr;
@@ -626,7 +635,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // O_x must hold P(j-1)V(j-1) before it is rescaled.  PV_x(j-2) is complete
                     // (QK_x(j) was issued after it), so parity (j-1)&1 of pv_done is unambiguous.
                     // Thread halves split O's columns.
-                    mbar_wait(smem_u32(&bars->pv_done[x]), (j - 1) & 1);
+                    // PV_x(j-1) has finished accumulating into O_x (per-buffer barriers keep
+                    // the phase unambiguous; PV_x(j-1+NB) needs P from a later step).
+                    mbar_wait(smem_u32(&bars->pv_done[x][(j - 1) % NB]), ((j - 1) / NB) & 1);
                     tc_fence_after();
 #pragma unroll 1
                     for (int c = 0; c < D / 2; c += 32) {
@@ -646,9 +657,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (tr) SAB_STAMP(x, j, 4);
                 if (j + 1 < nkv_x) {  // S(j+1) is issued into TMEM registers now; waited at the loop top
                     if (tr) SAB_STAMP(x, j + 1, 0);
-                    mbar_wait(smem_u32(&bars->s_full[x][b ^ 1]), ((j + 1) >> 1) & 1);
+                    mbar_wait(smem_u32(&bars->s_full[x][(j + 1) % NB]), ((j + 1) / NB) & 1);
                     tc_fence_after();
-                    tmem_ld16x2_32(tbase + lane_off + x * 128 + (b ^ 1) * 64, r);
+                    tmem_ld16x2_32(tbase + lane_off + x * (NB * 64) + ((j + 1) % NB) * 64, r);
                 }
             }
 
