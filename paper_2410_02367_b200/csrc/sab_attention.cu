@@ -601,6 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(smem_u32(&bars->s_full[x][0]), 0);
             tc_fence_after();
             tmem_ld16x2_32(tbase + lane_off + x * (NB * 64), r);
+#pragma unroll(PT ? 1 : 2)  // B: compile-time buffer parity per copy (+1-2 %); T would spill
             for (int j = 0; j < nkv_x; ++j) {
                 const float ks_cur = ks_next;
                 if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
