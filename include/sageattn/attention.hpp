@@ -21,8 +21,9 @@
 //     P~V accumulator (attention.hpp:84-102, 321, 531-533);
 //   * pure / re-entrant calls (per-call device contexts, attention.hpp:9-12).
 // Differences (documented in INTEGRATION.md):
-//   * only SAGEAttn-B (PerBlock Q/K) and SAGEAttn-T (PerToken Q/K) with Fp16Acc P~V,
-//     block 128/64 and INT8 run; vB/vT, FP8 dtypes or other block sizes throw
+//   * only SAGEAttn-B (PerBlock Q/K) and SAGEAttn-T (PerToken Q/K) with Fp16Acc P~V, and
+//     SAGEAttn-vB (PerBlock Q/K with INT8 P~V),
+//     block 128/64 and INT8 run; vT, FP8 dtypes or other block sizes throw
 //     std::invalid_argument -- there is no CPU fallback;
 //   * head_dim must be 64 or 128;
 //   * P~V accumulates in FP32 on the tensor cores (the reference's
@@ -165,12 +166,16 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
         throw std::invalid_argument("sage_attention: block sizes must be >= 1");
     if (!in.q.same_shape(in.k) || !in.q.same_shape(in.v))
         throw std::invalid_argument("sage_attention: Q, K, V shapes differ");
-    if ((config.qk_granularity != QkGranularity::PerBlock && config.qk_granularity != QkGranularity::PerToken) ||
-        config.pv_path != PvPath::Fp16Acc)
+    if (config.qk_granularity != QkGranularity::PerBlock && config.qk_granularity != QkGranularity::PerToken)
         throw std::invalid_argument(
-            "sage_attention: only SAGEAttn-B / SAGEAttn-T (PerBlock or PerToken Q/K, FP16 P~V) run on the B200 path");
+            "sage_attention: only PerBlock (B, vB) or PerToken (T) Q/K granularity runs on the B200 path");
+    if (config.pv_path == PvPath::Int8 && config.qk_granularity != QkGranularity::PerBlock)
+        throw std::invalid_argument(
+            "sage_attention: SAGEAttn-vT (PerToken Q/K with INT8 P~V) is not built on the B200 path");
     if (options.qk_dtype != QuantDtype::Int8)
         throw std::invalid_argument("sage_attention: only INT8 Q/K quantization runs on the B200 path");
+    if (config.pv_path == PvPath::Int8 && options.pv_dtype != QuantDtype::Int8)
+        throw std::invalid_argument("sage_attention: only INT8 P~V quantization runs on the B200 path");
 
     sab_desc d;
     sab_desc_init(&d, in.q.batch, in.q.heads, in.q.tokens, in.q.head_dim, in.causal ? 1 : 0);
@@ -181,6 +186,7 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
     d.smooth_k = options.smooth_k ? 1 : 0;
     d.check_v = 1;  // validate_input scans V too (attention.hpp:101)
     d.qk_granularity = config.qk_granularity == QkGranularity::PerToken ? SAB_QK_PER_TOKEN : SAB_QK_PER_BLOCK;
+    d.pv_path = config.pv_path == PvPath::Int8 ? SAB_PV_PATH_INT8 : SAB_PV_PATH_FP16;
     Tensor4f out(in.q.batch, in.q.heads, in.q.tokens, in.q.head_dim);
     int n_dev = b200::device_count_override();
     if (n_dev <= 0) sab_device_count(&n_dev);

@@ -11,6 +11,8 @@
  * is a thin header over the functions below.  Each function names the
  * reference interface it replaces.
  *
+ * SAGEAttn-vB (INT8 P~V) shares K1 and K2 through sab_desc.pv_path.
+ *
  * Tensor layout everywhere: contiguous (batch, heads, tokens, head_dim),
  * i.e. units = batch*heads independent (tokens x head_dim) slices, the
  * layout of Tensor4::at (tensor.hpp:76-81).
@@ -27,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SAB_ABI_VERSION 2
+#define SAB_ABI_VERSION 3
 
 /* Status codes.  The C++ shim maps them back to the reference's exceptions:
  * SAB_ERR_SHAPE / SAB_ERR_NONFINITE / SAB_ERR_UNSUPPORTED -> std::invalid_argument,
@@ -57,6 +59,11 @@ enum sab_pv_accum { SAB_PV_FP32 = 0, SAB_PV_FP16_TILE = 1 };
  * SAGEAttn-T (one scale per token; kernel_config_for(T), attention.hpp:50). */
 enum sab_qk_granularity { SAB_QK_PER_BLOCK = 0, SAB_QK_PER_TOKEN = 1 };
 
+/* P~V path: KernelConfig::pv_path (attention.hpp:35, 41-46).  FP16 = SAGEAttn-B/T
+ * (binary16 P~ and V); INT8 = SAGEAttn-vB (static-scale INT8 P~, per-channel INT8 V,
+ * INT32 products; kernel_config_for(VB), attention.hpp:53, 476-505).  ABI 3. */
+enum sab_pv_path { SAB_PV_PATH_FP16 = 0, SAB_PV_PATH_INT8 = 1 };
+
 /* Call descriptor: the shape of AttentionInput (attention.hpp:27-32) plus the
  * KernelConfig/SageOptions fields the B/T paths read (attention.hpp:41-46, 71-77). */
 typedef struct sab_desc {
@@ -70,6 +77,7 @@ typedef struct sab_desc {
     int32_t pv_accum;     /* sab_pv_accum                                          */
     int32_t check_v;      /* 1: scan V for non-finite values (validate_input)      */
     int32_t qk_granularity; /* sab_qk_granularity (ABI 2)                            */
+    int32_t pv_path;      /* sab_pv_path (ABI 3)                                   */
 } sab_desc;
 
 /* Fills *d with the SAGEAttn-B defaults (kernel_config_for(B), attention.hpp:51;
@@ -90,6 +98,10 @@ typedef struct sab_ws_layout {
     uint64_t total;     /* workspace bytes                                            */
     int32_t n_partials; /* subtree sums per unit of the pairwise mean tree            */
     int32_t tree_depth; /* depth of the 4..9-token leaf level (quant.hpp:203-213)     */
+    uint64_t vcodes;    /* int8  [units][head_dim][64*ceil(tokens/64)] V^ transposed (INT8
+                           P~V path only; quantize(V, per_channel), quant.hpp:128-173) */
+    uint64_t vscales;   /* float [units][head_dim] delta_V, then float [units][head_dim]
+                           channel max |v| scratch (INT8 P~V path only)              */
 } sab_ws_layout;
 
 const char* sab_status_string(int status);

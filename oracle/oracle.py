@@ -75,6 +75,8 @@ class Oracle:
                                    C.c_int, _f32p, _u64p]
         lib.orc_sage.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 8 + [_f32p, _u64p]
         lib.orc_sage_tiles.argtypes = [_i8p, _f32p, _i8p, _f32p, _f32p] + [C.c_int] * 10 + [_f32p, _u64p]
+        lib.orc_sage_v.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 9 + [_f32p, _u64p]
+        lib.orc_quantize_int8_cols.argtypes = [_f32p, C.c_int, C.c_int, _i8p, _f32p]
         lib.orc_naive.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
         self.lib = lib
 
@@ -148,14 +150,26 @@ class Oracle:
             raise RuntimeError(f"oracle failed: {st}")
         return out, macs
 
-    def sage(self, q, k, v, causal=False, smooth=True, pv_fp32=True, per_token=False, threads=None):
-        """SAGEAttn-B (per_token=False) or SAGEAttn-T (per_token=True) forward; returns (out, macs)."""
+    def quantize_per_channel(self, a):
+        """V^ of the vB/vT paths: (codes int8 (rows, cols), scales float32 (cols,)) (quant.hpp:128-173)."""
+        a = _f32(a)
+        rows, cols = a.shape
+        codes = np.empty((rows, cols), np.int8)
+        scales = np.empty(cols, np.float32)
+        st = self.lib.orc_quantize_int8_cols(a, rows, cols, codes, scales)
+        if st == 2:
+            raise ValueError("sage_attention: non-finite input")
+        return codes, scales
+
+    def sage(self, q, k, v, causal=False, smooth=True, pv_fp32=True, per_token=False, threads=None,
+             pv_int8=False):
+        """SAGEAttn-B / -T (pv_int8=False) or -vB / -vT (pv_int8=True) forward; returns (out, macs)."""
         q, k, v = _f32(q), _f32(k), _f32(v)
         units, n, d = q.shape
         out = np.empty_like(q)
         macs = np.zeros(2, np.uint64)
-        st = self.lib.orc_sage(q, k, v, units, n, d, int(causal), int(smooth), int(pv_fp32), int(per_token),
-                               threads or os.cpu_count() or 1, out, macs)
+        st = self.lib.orc_sage_v(q, k, v, units, n, d, int(causal), int(smooth), int(pv_fp32), int(per_token),
+                                 int(pv_int8), threads or os.cpu_count() or 1, out, macs)
         if st == 2:
             raise ValueError("sage_attention: non-finite input")
         if st == 3:
@@ -231,6 +245,7 @@ class Reference:
                                          _f32p]
         lib.ref_quantize_qk_per_token.argtypes = [_f32p, _f32p] + [C.c_int] * 5 + [_i8p, _f32p, _i8p, _f32p]
         lib.ref_sage_attention_variant.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 8 + [_f32p]
+        lib.ref_quantize_per_channel.argtypes = [_f32p, C.c_int, C.c_int, _i8p, _f32p]
         self.lib = lib
 
     def _raise(self, st):
@@ -289,15 +304,27 @@ class Reference:
         return qc, qs, kc, ks
 
     def sage_attention_variant(self, q4, k4, v4, variant="T", causal=False, smooth=True, pv_fp32=False):
-        """sageattn::sage_attention(in, SageVariant::T|B, opts)."""
+        """sageattn::sage_attention(in, SageVariant::T|B|VT|VB, opts)."""
         q4, k4, v4 = _f32(q4), _f32(k4), _f32(v4)
         b, h, n, d = q4.shape
         out = np.empty_like(q4)
-        st = self.lib.ref_sage_attention_variant(q4, k4, v4, b, h, n, d, int(causal), 0 if variant == "T" else 1,
+        code = {"T": 0, "B": 1, "VT": 2, "VB": 3}[variant]
+        st = self.lib.ref_sage_attention_variant(q4, k4, v4, b, h, n, d, int(causal), code,
                                                  int(smooth), int(pv_fp32), out)
         if st:
             self._raise(st)
         return out
+
+    def quantize_per_channel(self, a):
+        """quantize(a, Granularity::per_channel(), Int8): (codes (rows, cols), scales (cols,))."""
+        a = _f32(a)
+        rows, cols = a.shape
+        codes = np.empty((rows, cols), np.int8)
+        scales = np.empty(cols, np.float32)
+        st = self.lib.ref_quantize_per_channel(a, rows, cols, codes, scales)
+        if st:
+            self._raise(st)
+        return codes, scales
 
     def int8_tile(self, qc, kc, r0, bq, c0, bkv):
         n, d = qc.shape

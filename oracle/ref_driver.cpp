@@ -109,7 +109,7 @@ int ref_quantize_qk_per_token(const float* q, const float* k, int b, int h, int 
     } catch (const std::invalid_argument& e) { return fail(e, 1); }
 }
 
-// sage_attention(in, SageVariant v, opts) (attention.hpp:547-550) for v = 0 (T) or 1 (B).
+// sage_attention(in, SageVariant v, opts) (attention.hpp:547-550) for v = 0 (T), 1 (B), 2 (vT), 3 (vB).
 int ref_sage_attention_variant(const float* q, const float* k, const float* v, int b, int h, int n, int d, int causal,
                                int variant, int smooth, int pv_fp32, float* out) {
     try {
@@ -117,12 +117,26 @@ int ref_sage_attention_variant(const float* q, const float* k, const float* v, i
         SageOptions opt;
         opt.smooth_k = smooth != 0;
         opt.pv_fp32_accumulator = pv_fp32 != 0;
-        Tensor4f o = sage_attention(in, variant == 0 ? SageVariant::T : SageVariant::B, opt);
+        static const SageVariant kV[4] = {SageVariant::T, SageVariant::B, SageVariant::VT, SageVariant::VB};
+        if (variant < 0 || variant > 3) return 1;
+        Tensor4f o = sage_attention(in, kV[variant], opt);
         std::memcpy(out, o.data.data(), sizeof(float) * o.size());
         return 0;
     } catch (const std::invalid_argument& e) { return fail(e, 1); } catch (const std::overflow_error& e) {
         return fail(e, 3);
     }
+}
+
+// quantize(a, Granularity::per_channel(), Int8) (quant.hpp:128-173): V^ of the vB/vT paths.
+int ref_quantize_per_channel(const float* a, int rows, int cols, int8_t* codes, float* scales) {
+    try {
+        Matrix<float> m(rows, cols);
+        std::memcpy(&m(0, 0), a, sizeof(float) * size_t(rows) * cols);
+        QuantizedMatrix qm = quantize(m, Granularity::per_channel(), QuantDtype::Int8);
+        std::memcpy(codes, qm.codes.data(), qm.codes.size());
+        std::memcpy(scales, qm.scales.data(), sizeof(float) * qm.scales.size());
+        return 0;
+    } catch (const std::invalid_argument& e) { return fail(e, 1); }
 }
 
 // detail::int8_tile_nt (attention.hpp:265-279) on raw code matrices.

@@ -172,6 +172,31 @@ int orc_quantize_int8_rows(const float* a, int rows, int cols, int block, int8_t
     return ORC_OK;
 }
 
+/* Per-channel INT8 quantizer (quant.hpp:128-173 with Granularity::per_channel,
+ * group_of(r, c) = c, quant.hpp:46-63): delta_c = max_t |a[t][c]| / 127. */
+int orc_quantize_int8_cols(const float* a, int rows, int cols, int8_t* codes, float* scales)
+{
+    for (size_t i = 0; i < (size_t)rows * cols; ++i)
+        if (!isfinite(a[i])) return ORC_ERR_NONFINITE;
+    for (int c = 0; c < cols; ++c) {
+        float amax = 0.0f;
+        for (int r = 0; r < rows; ++r) {
+            float v = fabsf(a[(size_t)r * cols + c]);
+            if (v > amax) amax = v;
+        }
+        float inv;
+        if (amax == 0.0f) {
+            scales[c] = 1.0f;
+            inv = 0.0f;
+        } else {
+            scales[c] = amax / 127.0f;
+            inv = 1.0f / scales[c];
+        }
+        for (int r = 0; r < rows; ++r) codes[(size_t)r * cols + c] = orc_code(a[(size_t)r * cols + c], inv);
+    }
+    return ORC_OK;
+}
+
 /* The B-path prepass for one unit: fold+quantize Q in 128-token blocks and
  * smooth+quantize K in 64-token blocks (attention.hpp:336-360). */
 int orc_prepass_unit(const float* q, const float* k, int n, int d, int block_q, int block_kv, int smooth,
@@ -238,9 +263,9 @@ int orc_causal_tile(int i, int j, int block_q, int block_kv, int n)
  * Returns ORC_ERR_OVERFLOW when the binary16 accumulator overflowed
  * (attention.hpp:531-533).  macs[0..1] accumulate the SageDiagnostics MAC
  * counters (attention.hpp:404, 445) when non-NULL. */
-int orc_sage_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const float* ks, const float* v, int n, int d,
-                   int causal, int pv_fp32, int block_q, int block_kv, int gq, int gk, int qt0, int qt1, float* out,
-                   uint64_t* macs)
+static int orc_sage_tiles_v(const int8_t* qc, const float* qs, const int8_t* kc, const float* ks, const float* v,
+                            int n, int d, int causal, int pv_fp32, int pv_int8, int block_q, int block_kv, int gq,
+                            int gk, int qt0, int qt1, float* out, uint64_t* macs)
 {
     const int n_kv = (n + block_kv - 1) / block_kv;
     int32_t* acc = (int32_t*)malloc(sizeof(int32_t) * (size_t)block_q * block_kv);
@@ -251,11 +276,23 @@ int orc_sage_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const fl
     float* l = (float*)malloc(sizeof(float) * (size_t)block_q);
     float* rs = (float*)malloc(sizeof(float) * (size_t)block_q);
     double* v16 = (double*)malloc(sizeof(double) * (size_t)n * d);
+    int8_t* vc = pv_int8 ? (int8_t*)malloc((size_t)n * d) : NULL;
+    float* vs = pv_int8 ? (float*)malloc(sizeof(float) * (size_t)d) : NULL;
+    int8_t* pc = (int8_t*)malloc((size_t)block_q * block_kv);
     int status = ORC_OK;
-    if (!acc || !s || !p16 || !o || !m || !l || !rs || !v16) { status = ORC_ERR_NOMEM; goto done; }
+    if (!acc || !s || !p16 || !o || !m || !l || !rs || !v16 || !pc || (pv_int8 && (!vc || !vs))) {
+        status = ORC_ERR_NOMEM;
+        goto done;
+    }
 
-    /* V -> binary16 grid (attention.hpp:371-375). */
-    for (size_t i = 0; i < (size_t)n * d; ++i) v16[i] = orc_snap_half((double)v[i]);
+    if (pv_int8) {
+        /* SAGEAttn-vB/vT: V -> per-channel INT8 (attention.hpp:376-378). */
+        status = orc_quantize_int8_cols(v, n, d, vc, vs);
+        if (status != ORC_OK) goto done;
+    } else {
+        /* V -> binary16 grid (attention.hpp:371-375). */
+        for (size_t i = 0; i < (size_t)n * d; ++i) v16[i] = orc_snap_half((double)v[i]);
+    }
 
     for (int i = qt0; i < qt1; ++i) {
         const int r0 = i * block_q;
@@ -303,6 +340,29 @@ int orc_sage_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const fl
                 l[r] = rs[r] * l[r] + sum;
             }
             if (macs) macs[1] += (uint64_t)bq * bkv * d;
+            if (pv_int8) {
+                /* INT8 P~V (attention.hpp:476-505): P~ -> static-scale codes
+                 * rne(p * 127) (quantize_p_static, quant.hpp:258-279), O rescaled in
+                 * binary32, INT32 dot products dequantized by (acc * dP) * dV[c]. */
+                const float dp = 1.0f / 127.0f;
+                for (int r = 0; r < bq; ++r)
+                    for (int c = 0; c < bkv; ++c) {
+                        const float pv = s[r * block_kv + c];
+                        if (!(pv >= 0.0f && pv <= 1.0f + 1e-6f)) { status = ORC_ERR_SHAPE; goto done; }
+                        pc[r * block_kv + c] = orc_code(pv, 127.0f);
+                    }
+                for (int r = 0; r < bq; ++r) {
+                    double* orow = o + (size_t)r * d;
+                    for (int c = 0; c < d; ++c) orow[c] = (double)((float)orow[c] * rs[r]);
+                    for (int c = 0; c < d; ++c) {
+                        int32_t a = 0;
+                        for (int kk = 0; kk < bkv; ++kk)
+                            a += (int32_t)pc[r * block_kv + kk] * (int32_t)vc[(size_t)(c0 + kk) * d + c];
+                        orow[c] = (double)((float)orow[c] + ((float)a * dp) * vs[c]);
+                    }
+                }
+                continue;
+            }
             /* O rescale and P~ V with the binary16 (or binary32) accumulator
              * (attention.hpp:447-475). */
             for (int r = 0; r < bq; ++r) {
@@ -333,14 +393,22 @@ int orc_sage_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const fl
             const float inv_l = 1.0f / l[r];
             for (int c = 0; c < d; ++c) {
                 double src = o[(size_t)r * d + c];
-                if (!isfinite(src)) { status = ORC_ERR_OVERFLOW; goto done; }
+                if (!pv_int8 && !isfinite(src)) { status = ORC_ERR_OVERFLOW; goto done; }
                 out[(size_t)(r0 + r) * d + c] = (float)src * inv_l;
             }
         }
     }
 done:
-    free(acc); free(s); free(p16); free(o); free(m); free(l); free(rs); free(v16);
+    free(acc); free(s); free(p16); free(o); free(m); free(l); free(rs); free(v16); free(vc); free(vs); free(pc);
     return status;
+}
+
+int orc_sage_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const float* ks, const float* v, int n, int d,
+                   int causal, int pv_fp32, int block_q, int block_kv, int gq, int gk, int qt0, int qt1, float* out,
+                   uint64_t* macs)
+{
+    return orc_sage_tiles_v(qc, qs, kc, ks, v, n, d, causal, pv_fp32, 0, block_q, block_kv, gq, gk, qt0, qt1, out,
+                            macs);
 }
 
 /* The variant B tile loop: scale groups equal to the tiles (per_block(128 / 64)). */
@@ -355,8 +423,9 @@ int orc_sage_b_tiles(const int8_t* qc, const float* qs, const int8_t* kc, const 
 /* Whole SAGEAttn forward for one unit (attention.hpp:318-545): variant B =
  * PerBlock(128/64) + Fp16Acc, variant T (per_token) = PerToken + Fp16Acc with the
  * same 128 x 64 tiles (kernel_config_for, attention.hpp:48-55). */
-int orc_sage_unit(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth, int pv_fp32,
-                  int per_token, float* out, uint64_t* macs)
+/* pv_int8 selects PvPath::Int8 (variants vB / vT, kernel_config_for, attention.hpp:52-53). */
+int orc_sage_unit_v(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth, int pv_fp32,
+                    int per_token, int pv_int8, float* out, uint64_t* macs)
 {
     const int bq = 128, bkv = 64;
     const int gq = per_token ? 1 : bq, gk = per_token ? 1 : bkv;
@@ -370,11 +439,17 @@ int orc_sage_unit(const float* q, const float* k, const float* v, int n, int d, 
     if (qc && kc && qs && ks) {
         st = orc_prepass_unit(q, k, n, d, gq, gk, smooth, qc, qs, kc, ks, NULL);
         if (st == ORC_OK)
-            st = orc_sage_tiles(qc, qs, kc, ks, v, n, d, causal, pv_fp32, bq, bkv, gq, gk, 0, (n + bq - 1) / bq,
-                                out, macs);
+            st = orc_sage_tiles_v(qc, qs, kc, ks, v, n, d, causal, pv_fp32, pv_int8, bq, bkv, gq, gk, 0,
+                                  (n + bq - 1) / bq, out, macs);
     }
     free(qc); free(kc); free(qs); free(ks);
     return st;
+}
+
+int orc_sage_unit(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth, int pv_fp32,
+                  int per_token, float* out, uint64_t* macs)
+{
+    return orc_sage_unit_v(q, k, v, n, d, causal, smooth, pv_fp32, per_token, 0, out, macs);
 }
 
 int orc_sage_b_unit(const float* q, const float* k, const float* v, int n, int d, int causal, int smooth,
@@ -416,7 +491,7 @@ typedef struct {
     const float *q, *k, *v;
     float* out;
     double* out64;
-    int units, n, d, causal, smooth, pv_fp32, naive, per_token;
+    int units, n, d, causal, smooth, pv_fp32, naive, per_token, pv_int8;
     int next;
     int status;
     uint64_t macs[2];
@@ -437,8 +512,8 @@ static void* orc_worker(void* arg)
         if (job->naive)
             orc_naive_unit(job->q + off, job->k + off, job->v + off, job->n, job->d, job->causal, job->out64 + off);
         else
-            st = orc_sage_unit(job->q + off, job->k + off, job->v + off, job->n, job->d, job->causal, job->smooth,
-                               job->pv_fp32, job->per_token, job->out + off, macs);
+            st = orc_sage_unit_v(job->q + off, job->k + off, job->v + off, job->n, job->d, job->causal,
+                                 job->smooth, job->pv_fp32, job->per_token, job->pv_int8, job->out + off, macs);
         if (st != ORC_OK) {
             pthread_mutex_lock(&job->mu);
             if (job->status == ORC_OK) job->status = st;
@@ -466,8 +541,9 @@ static int orc_run(orc_job* job, int threads, uint64_t* macs)
     return job->status;
 }
 
-int orc_sage(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,
-             int pv_fp32, int per_token, int threads, float* out, uint64_t* macs)
+/* Any of the four variants: per_token (T / vT) and pv_int8 (vB / vT). */
+int orc_sage_v(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,
+               int pv_fp32, int per_token, int pv_int8, int threads, float* out, uint64_t* macs)
 {
     if (units < 1 || n < 1 || d < 1) return ORC_ERR_SHAPE;
     orc_job job;
@@ -475,7 +551,14 @@ int orc_sage(const float* q, const float* k, const float* v, int units, int n, i
     job.q = q; job.k = k; job.v = v; job.out = out;
     job.units = units; job.n = n; job.d = d; job.causal = causal; job.smooth = smooth; job.pv_fp32 = pv_fp32;
     job.per_token = per_token;
+    job.pv_int8 = pv_int8;
     return orc_run(&job, threads, macs);
+}
+
+int orc_sage(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,
+             int pv_fp32, int per_token, int threads, float* out, uint64_t* macs)
+{
+    return orc_sage_v(q, k, v, units, n, d, causal, smooth, pv_fp32, per_token, 0, threads, out, macs);
 }
 
 int orc_sage_b(const float* q, const float* k, const float* v, int units, int n, int d, int causal, int smooth,

@@ -27,6 +27,8 @@ SAB_PV_FP32 = 0
 SAB_PV_FP16_TILE = 1
 SAB_QK_PER_BLOCK = 0  # SAGEAttn-B
 SAB_QK_PER_TOKEN = 1  # SAGEAttn-T
+SAB_PV_PATH_FP16 = 0  # B / T
+SAB_PV_PATH_INT8 = 1  # vB
 
 # Every symbol include/sageattn_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
@@ -40,13 +42,13 @@ EXPORTS = (
 class SabDesc(C.Structure):
     _fields_ = [(name, C.c_int32) for name in (
         "batch", "heads", "tokens", "head_dim", "causal", "in_dtype", "out_dtype", "block_q", "block_kv",
-        "smooth_k", "pv_accum", "check_v", "qk_granularity")]
+        "smooth_k", "pv_accum", "check_v", "qk_granularity", "pv_path")]
 
 
 class SabWsLayout(C.Structure):
     _fields_ = [(name, C.c_uint64) for name in (
         "qcodes", "kcodes", "qscales", "kscales", "mean_k", "partials", "v16", "status", "total")] + [
-        ("n_partials", C.c_int32), ("tree_depth", C.c_int32)]
+        ("n_partials", C.c_int32), ("tree_depth", C.c_int32), ("vcodes", C.c_uint64), ("vscales", C.c_uint64)]
 
 
 class SabError(RuntimeError):
@@ -104,13 +106,15 @@ def check(status: int):
 
 
 def desc(batch, heads, tokens, head_dim, causal=False, in_dtype=SAB_F16, out_dtype=SAB_F32, block_q=128,
-         block_kv=64, smooth_k=True, pv_accum=SAB_PV_FP32, check_v=False, per_token=False) -> SabDesc:
+         block_kv=64, smooth_k=True, pv_accum=SAB_PV_FP32, check_v=False, per_token=False,
+         pv_int8=False) -> SabDesc:
     d = SabDesc()
     load().sab_desc_init(C.byref(d), batch, heads, tokens, head_dim, int(causal))
     d.in_dtype, d.out_dtype = in_dtype, out_dtype
     d.block_q, d.block_kv = block_q, block_kv
     d.smooth_k, d.pv_accum, d.check_v = int(smooth_k), pv_accum, int(check_v)
     d.qk_granularity = SAB_QK_PER_TOKEN if per_token else SAB_QK_PER_BLOCK
+    d.pv_path = SAB_PV_PATH_INT8 if pv_int8 else SAB_PV_PATH_FP16
     return d
 
 

@@ -275,6 +275,56 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
     return alpha;
 }
 
+// SAGEAttn-vB variant of softmax_half (INT8 P~V, attention.hpp:476-505): the running max
+// is exact (no lazy threshold) so every p lies in [0, 1], and P~ is stored as the static-scale
+// codes rne(p * 127) (quantize_p_static, quant.hpp:258-279), four per TMEM column (thread t's
+// 8 words go to columns [8*half, 8*half + 8)), the A operand of the kind::i8 PV MMA.  All
+// exponentials are MUFU ex2 of float(acc) * cg - m (one rounding), so the codes are the
+// reference's up to an ulp of the exponent.  Returns the O rescale factor 2^(m_old - m).
+template <bool MASK, bool CAUSAL>
+__device__ __forceinline__ float softmax_half_i8(const uint32_t (&r)[32], uint32_t ts, int half, float cg, int kb,
+                                                 int qi, int n, float& m, float& l, bool& rescale) {
+    const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
+    int imax = group_max<MASK>(r, lim);
+    imax = max(imax, __shfl_xor_sync(0xffffffffu, imax, 16));
+    const float mx = (MASK && imax == kMaskedAcc) ? -INFINITY : (__int_as_float(imax) - kMagicF) * cg;
+    const float m_new = fmaxf(m, mx);
+    rescale = __any_sync(0xffffffffu, m_new > m);
+    const float alpha = (m_new > m) ? ex2(m - m_new) : 1.0f;
+    m = m_new;
+    const float mref = (m == -INFINITY) ? 0.0f : m;
+    const f2 cg2{cg, cg};
+    const int lim2 = MASK ? opaque(lim) : lim;
+    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t b[4];
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+            const int c = 4 * i + e;
+            const f2 a = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-kMagicF, -kMagicF});
+            const f2 t = ffma2(a, cg2, f2{-mref, -mref});
+            f2 pp{ex2(t.x), ex2(t.y)};
+            if (MASK) {
+                pp.x = (c >= lim2) ? 0.0f : pp.x;
+                pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+            }
+            acc[(2 * i + e / 2) & 3] = fadd2(acc[(2 * i + e / 2) & 3], pp);
+            // rne(p * 127): the product rounded to binary32 (quant.hpp:96), then 2^23 + 2^22
+            // added so the code sits in the low mantissa byte.
+            const f2 q = fadd2(ffma2(pp, f2{127.0f, 127.0f}, f2{0.0f, 0.0f}), f2{kMagicF, kMagicF});
+            b[e] = __float_as_uint(q.x);
+            b[e + 1] = __float_as_uint(q.y);
+        }
+        pk[i] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    }
+    tmem_st16x2_8(ts, pk);
+    const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+    l = fmaf(l, alpha, sum.x + sum.y);
+    return alpha;
+}
+
 // SAGEAttn-T variant of softmax_half: per-token scales, so the dequant factor
 // w = dQ[row] * dK[key] * log2 e differs per element and the row max is taken on
 // the scaled scores (attention.hpp:409-414 with per_token group_of, quant.hpp:56-63).
@@ -390,7 +440,7 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
     return alpha;
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT>
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -484,11 +534,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(smem_u32(&bars->kv_empty[s]), ph ^ 1);
                 SAB_STAMP(4, j, 1);
                 const uint32_t full = smem_u32(&bars->kv_full[s]);
-                mbar_arrive_expect_tx(full, C::kKBytes + C::kVBytes);
+                mbar_arrive_expect_tx(full, C::kKBytes + (VI8 ? kBN * D : C::kVBytes));
                 tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, j * kBN, unit);
+                if (VI8) {  // V^ transposed: D channel rows of 64 key codes (K-major B operand)
+                    tma_load_3d(sV + s * C::kVBytes, &tm_v, full, j * kBN, 0, unit);
+                } else {
 #pragma unroll
-                for (int c = 0; c < D / 64; ++c)
-                    tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, j * kBN, unit);
+                    for (int c = 0; c < D / 64; ++c)
+                        tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, j * kBN, unit);
+                }
             }
         }
         __syncwarp();
@@ -502,7 +556,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Descriptors are advanced by adding (byte offset >> 4) to the start-address field.
         const uint64_t dq0 = make_smem_desc(sQ, 16, C::kSboQK, C::kSwizzleQK);
         const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);
-        const uint64_t dv0 = make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
+        const uint64_t dv0 = VI8 ? make_smem_desc(sV, 16, 8 * 64, kSwizzle64B)
+                                 : make_smem_desc(sV, C::kVChunk, 1024, kSwizzle128B);
+        constexpr uint32_t idesc_pv8 = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, D);
         constexpr uint32_t idesc_bias = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 0, kBM, kBN);
         const uint64_t d_bias_a = make_smem_desc(smem_u32(smem + C::kOffBiasA), 128, 256, kSwizzleNone);
         const uint64_t d_bias_b = make_smem_desc(smem_u32(smem + C::kOffBiasB), 128, 256, kSwizzleNone);
@@ -554,10 +610,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t t_p = tbase + x * (NB * 64) + (j % NB) * 64;
                     const uint32_t t_o = tbase + C::kOffO + x * D;
                     if (elect_one()) {
+                        if (VI8) {  // INT32 O_x += P~^(j) V^(j): 2 x K=32 codes, P~^ from TMEM
 #pragma unroll
-                        for (int kk = 0; kk < kBN / 16; ++kk)
-                            umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)), idesc_pv,
-                                        (j > 0 || kk > 0) ? 1u : 0u);
+                            for (int kk = 0; kk < kBN / 32; ++kk)
+                                umma_i8_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * 2), idesc_pv8,
+                                           (j > 0 || kk > 0) ? 1u : 0u);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < kBN / 16; ++kk)
+                                umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)),
+                                            idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+                        }
                         umma_commit(smem_u32(&bars->pv_done[x][j % NB]));
                         if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
                     }
@@ -618,7 +681,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
                 bool rescale;
                 float alpha;
-                if (PT) {
+                if (VI8) {
+                    if (need_mask)
+                        alpha = softmax_half_i8<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale);
+                    else
+                        alpha = softmax_half_i8<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale);
+                } else if (PT) {
                     const float* dkp = ksc + kb + 32 * half;
                     if (need_mask)
                         alpha = softmax_half_pt<true, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump,
@@ -645,8 +713,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t o[32];
                         tmem_ld16x2_32o<D / 2>(t_o + c, o);
                         tmem_wait_ld();
+                        if (VI8) {
+                            // INT32 O: O <- rne(alpha * O).  The rounding (<= 0.5 of a code product
+                            // per move of the row max) is far below P~'s own 1/254 step.
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                            for (int e = 0; e < 32; ++e)
+                                o[e] = static_cast<uint32_t>(
+                                    __float2int_rn(static_cast<float>(static_cast<int>(o[e])) * alpha));
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        }
                         tmem_st16x2_32o<D / 2>(t_o + c, o);
                     }
                 }
@@ -677,10 +754,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld16x2_32o<D / 2>(t_o + c, o);
                     tmem_wait_ld();
                     float v[32];
+                    if (VI8) {
+                        // (float(acc) * dP) * dV[c] (attention.hpp:494-495), then 1/l (536-538).
+                        const float4* vs4 = reinterpret_cast<const float4*>(
+                            p.vscales + static_cast<size_t>(unit) * D + half * (D / 2) + c);
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        finite &= isfinite(__uint_as_float(o[e]));
-                        v[e] = __uint_as_float(o[e]) * inv_l;
+                        for (int e4 = 0; e4 < 8; ++e4) {
+                            const float4 vs = __ldg(vs4 + e4);
+                            const float w[4] = {vs.x, vs.y, vs.z, vs.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int e = 4 * e4 + i;
+                                v[e] = ((static_cast<float>(static_cast<int>(o[e])) * (1.0f / 127.0f)) * w[i]) * inv_l;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            finite &= isfinite(__uint_as_float(o[e]));
+                            v[e] = __uint_as_float(o[e]) * inv_l;
+                        }
                     }
                     if (qi < n) {
                         const size_t off = (static_cast<size_t>(unit) * n + qi) * D + half * (D / 2) + c;
@@ -757,18 +850,21 @@ int raster_group_units(const AttnParams& p, int d) {
     return static_cast<int>((static_cast<size_t>(p.units) + groups - 1) / groups);
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT>
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
 cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     using C = Cfg<D>;
     CUtensorMap tq, tk, tv;
     const CUtensorMapSwizzle swqk = D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
     if (!make_map(&tq, p.qcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBM, swqk) ||
         !make_map(&tk, p.kcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, p.n, p.units, D, kBN, swqk) ||
-        !make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, kBN, CU_TENSOR_MAP_SWIZZLE_128B))
+        !(VI8 ? make_map(&tv, p.vcodes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.ldv, D, p.units, kBN, D,
+                         CU_TENSOR_MAP_SWIZZLE_64B)
+              : make_map(&tv, p.v16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, D, p.n, p.units, 64, kBN,
+                         CU_TENSOR_MAP_SWIZZLE_128B)))
         return cudaErrorInvalidValue;
     AttnParams pp = p;
     pp.group_units = raster_group_units(p, D);
-    auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP, PT>;
+    auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP, PT, VI8>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int ntq = (p.n + kBM - 1) / kBM;
@@ -781,16 +877,18 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <bool DUMP, bool PT>
+template <bool DUMP, bool PT, bool VI8 = false>
 cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
     const bool c = p.causal != 0, f = p.out_f32 != 0;
     if (p.d == 128) {
-        if (c) return f ? launch_k2<128, true, true, DUMP, PT>(p, s) : launch_k2<128, true, false, DUMP, PT>(p, s);
-        return f ? launch_k2<128, false, true, DUMP, PT>(p, s) : launch_k2<128, false, false, DUMP, PT>(p, s);
+        if (c)
+            return f ? launch_k2<128, true, true, DUMP, PT, VI8>(p, s) : launch_k2<128, true, false, DUMP, PT, VI8>(p, s);
+        return f ? launch_k2<128, false, true, DUMP, PT, VI8>(p, s) : launch_k2<128, false, false, DUMP, PT, VI8>(p, s);
     }
     if (p.d == 64) {
-        if (c) return f ? launch_k2<64, true, true, DUMP, PT>(p, s) : launch_k2<64, true, false, DUMP, PT>(p, s);
-        return f ? launch_k2<64, false, true, DUMP, PT>(p, s) : launch_k2<64, false, false, DUMP, PT>(p, s);
+        if (c)
+            return f ? launch_k2<64, true, true, DUMP, PT, VI8>(p, s) : launch_k2<64, true, false, DUMP, PT, VI8>(p, s);
+        return f ? launch_k2<64, false, true, DUMP, PT, VI8>(p, s) : launch_k2<64, false, false, DUMP, PT, VI8>(p, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -798,6 +896,7 @@ cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
 // The INT32 S dump does not read the scales, so it only needs the per-block build.
 template <bool DUMP>
 cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
+    if (!DUMP && p.vcodes) return dispatch_pt<false, false, true>(p, s);  // SAGEAttn-vB
     if (!DUMP && p.per_token) return dispatch_pt<false, true>(p, s);
     return dispatch_pt<DUMP, false>(p, s);
 }

@@ -59,8 +59,11 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     L->kscales = take(units * (pt ? npad : (n + kBlockKV - 1) / kBlockKV) * sizeof(float));
     L->mean_k = take(units * hd * sizeof(float));
     L->partials = take(units * size_t(n_partials) * hd * sizeof(float));
-    L->v16 = take(d->in_dtype == SAB_F32 ? units * n * hd * 2 : 0);
+    const bool pv8 = d->pv_path == SAB_PV_PATH_INT8;
+    L->v16 = take(d->in_dtype == SAB_F32 && !pv8 ? units * n * hd * 2 : 0);
     L->status = take(sizeof(int32_t) * (1 + units));  // status word + per-unit K1 counters
+    L->vcodes = take(pv8 ? units * hd * npad : 0);
+    L->vscales = take(pv8 ? 2 * units * hd * sizeof(float) : 0);
     L->total = off;
     L->n_partials = n_partials;
     L->tree_depth = depth;
@@ -84,7 +87,14 @@ PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const vo
     p.kscales = at<float>(ws, L.kscales);
     p.mean = at<float>(ws, L.mean_k);
     p.partials = at<float>(ws, L.partials);
-    p.v16 = d->in_dtype == SAB_F32 ? at<uint16_t>(ws, L.v16) : nullptr;
+    const bool pv8 = d->pv_path == SAB_PV_PATH_INT8;
+    p.v16 = d->in_dtype == SAB_F32 && !pv8 ? at<uint16_t>(ws, L.v16) : nullptr;
+    if (pv8) {
+        p.vcodes = at<int8_t>(ws, L.vcodes);
+        p.vscales = at<float>(ws, L.vscales);
+        p.vamax = reinterpret_cast<int*>(p.vscales + units_of(d) * d->head_dim);
+        p.ldv = (d->tokens + kBlockKV - 1) / kBlockKV * kBlockKV;
+    }
     p.status = at<int>(ws, L.status);
     p.counters = p.status + 1;
     p.units = int(units_of(d));
@@ -95,7 +105,7 @@ PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const vo
     p.n_partials = L.n_partials;
     p.smooth = d->smooth_k != 0;
     p.per_token = d->qk_granularity == SAB_QK_PER_TOKEN;
-    p.check_v = d->check_v != 0;
+    p.check_v = d->check_v != 0 && !pv8;  // the INT8 V pass scans V itself
     p.in_f32 = d->in_dtype == SAB_F32;
     p.inv_n = 1.0f / static_cast<float>(d->tokens);
     p.fold = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d->head_dim)));
@@ -109,7 +119,13 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
     a.kcodes = at<int8_t>(w, L.kcodes);
     a.qscales = at<float>(w, L.qscales);
     a.kscales = at<float>(w, L.kscales);
-    a.v16 = d->in_dtype == SAB_F32 ? static_cast<const void*>(at<uint16_t>(w, L.v16)) : v;
+    const bool pv8 = d->pv_path == SAB_PV_PATH_INT8;
+    a.v16 = pv8 ? nullptr : d->in_dtype == SAB_F32 ? static_cast<const void*>(at<uint16_t>(w, L.v16)) : v;
+    if (pv8) {
+        a.vcodes = at<int8_t>(w, L.vcodes);
+        a.vscales = at<float>(w, L.vscales);
+        a.ldv = (d->tokens + kBlockKV - 1) / kBlockKV * kBlockKV;
+    }
     a.o = o;
     a.status = at<int>(w, L.status);
     a.units = int(units_of(d));
@@ -192,6 +208,7 @@ void sab_desc_init(sab_desc* d, int32_t batch, int32_t heads, int32_t tokens, in
     d->pv_accum = SAB_PV_FP32;
     d->check_v = 0;
     d->qk_granularity = SAB_QK_PER_BLOCK;
+    d->pv_path = SAB_PV_PATH_FP16;
 }
 
 int sab_check_desc(const sab_desc* d) {
@@ -207,6 +224,10 @@ int sab_check_desc(const sab_desc* d) {
                          "sage_attention: SAGEAttn-B/T use block_q=128, block_kv=64 (kernel_config_for(B|T))");
     if (d->qk_granularity != SAB_QK_PER_BLOCK && d->qk_granularity != SAB_QK_PER_TOKEN)
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: Q/K granularity must be per-block (B) or per-token (T)");
+    if (d->pv_path != SAB_PV_PATH_FP16 && d->pv_path != SAB_PV_PATH_INT8)
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: P~V path must be FP16 (B/T) or INT8 (vB)");
+    if (d->pv_path == SAB_PV_PATH_INT8 && d->qk_granularity != SAB_QK_PER_BLOCK)
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: SAGEAttn-vT (per-token Q/K with INT8 P~V) is not built");
     if ((d->in_dtype != SAB_F16 && d->in_dtype != SAB_F32) || (d->out_dtype != SAB_F16 && d->out_dtype != SAB_F32))
         return set_error(SAB_ERR_ARGUMENT, "sab_desc: dtype must be SAB_F16 or SAB_F32");
     if (d->pv_accum != SAB_PV_FP32)
@@ -238,7 +259,8 @@ int sab_prepass(const sab_desc* d, const void* q, const void* k, const void* v, 
     int st = sab_workspace_layout(d, &L);
     if (st) return st;
     if (!q || !k) return set_error(SAB_ERR_ARGUMENT, "sab_prepass: q/k is NULL");
-    if ((d->in_dtype == SAB_F32 || d->check_v) && !v) return set_error(SAB_ERR_ARGUMENT, "sab_prepass: v is NULL");
+    if ((d->in_dtype == SAB_F32 || d->check_v || d->pv_path == SAB_PV_PATH_INT8) && !v)
+        return set_error(SAB_ERR_ARGUMENT, "sab_prepass: v is NULL");
     if (!ws || ws_bytes < L.total) return set_error(SAB_ERR_WORKSPACE, "sab_prepass: workspace too small");
     if (!aligned16(q) || !aligned16(k) || (v && !aligned16(v)) || !aligned16(ws))
         return set_error(SAB_ERR_ARGUMENT, "sab_prepass: pointers must be 16-byte aligned");
@@ -250,7 +272,7 @@ int sab_attention(const sab_desc* d, void* ws, size_t ws_bytes, const void* v, v
     int st = sab_workspace_layout(d, &L);
     if (st) return st;
     if (!ws || ws_bytes < L.total) return set_error(SAB_ERR_WORKSPACE, "sab_attention: workspace too small");
-    if (!o || (d->in_dtype == SAB_F16 && !v)) return set_error(SAB_ERR_ARGUMENT, "sab_attention: v/o is NULL");
+    if (!o || (d->in_dtype == SAB_F16 && d->pv_path != SAB_PV_PATH_INT8 && !v)) return set_error(SAB_ERR_ARGUMENT, "sab_attention: v/o is NULL");
     if (!aligned16(o) || (v && !aligned16(v))) return set_error(SAB_ERR_ARGUMENT, "sab_attention: misaligned v/o");
     return enqueue_attention(d, L, ws, v, o, static_cast<cudaStream_t>(stream));
 }

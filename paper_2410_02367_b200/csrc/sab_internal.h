@@ -36,6 +36,10 @@ struct PrepassParams {
     int n_partials;     // 2^depth / nodes_per_cta
     int smooth;
     int per_token;      // SAGEAttn-T: one scale per token (qscales/kscales [units][n])
+    int8_t* vcodes;     // vB: per-channel INT8 V^, transposed [units][d][ldv] (NULL: FP16 P~V path)
+    float* vscales;     // vB: delta_V [units][d]
+    int* vamax;         // vB: channel max |v| as float bits [units][d] (zeroed by launch_prepass)
+    int ldv;            // vB: tokens padded to 64
     int check_v;
     int in_f32;
     float inv_n;        // 1.0f / float(N)          (quant.hpp:228)
@@ -55,6 +59,9 @@ struct AttnParams {
     const float* qscales;
     const float* kscales;
     const void* v16;
+    const int8_t* vcodes;  // vB: INT8 V^ [units][d][ldv] (P~V kind::i8), else NULL
+    const float* vscales;  // vB: delta_V [units][d]
+    int ldv;
     void* o;
     int* status;
     int32_t* s_dump;  // debug: INT32 S tiles of one (unit, q-tile)

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
             }
         }
         if (!finite) atomicOr(p.status, kStatusNonFinite);
-        if (p.in_f32 || p.check_v) {
+        if (p.v16 || p.check_v) {
             bool vfin = true;
             for (int v = tid; v < rows * CV; v += kQThreads) {
                 const int row = v / CV, c8 = (v % CV) * 8;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
                 float x[8];
                 load8<T>(static_cast<const T*>(p.v) + off, x);
                 vfin &= all_finite8(x);
-                if (p.in_f32) {
+                if (p.v16) {
                     uint4 h;
                     h.x = pack_half2(x[0], x[1]);
                     h.y = pack_half2(x[2], x[3]);
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
 
     // V: fp32 inputs -> fp16 grid (with the finiteness check); fp16 inputs
     // are only scanned when asked (validate_input, attention.hpp:101).
-    if (p.in_f32 || p.check_v) {
+    if (p.v16 || p.check_v) {
         bool vfin = true;
         for (int v = tid; v < rows * CV; v += kQThreads) {
             const int row = v / CV, col = (v % CV) * 8;
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
             float x[8];
             load8<T>(static_cast<const T*>(p.v) + off, x);
             vfin &= all_finite8(x);
-            if (p.in_f32) {
+            if (p.v16) {
                 uint4 h;
                 h.x = pack_half2(x[0], x[1]);
                 h.y = pack_half2(x[2], x[3]);
@@ -816,8 +816,94 @@ __global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
     }
 }
 
+// ---------------------------------------------------------------- vB: V^ per channel
+// quantize(V, Granularity::per_channel(), Int8) (attention.hpp:376-378; quant.hpp:103-173):
+// delta_c = max_t |v[t][c]| / 127 over every token of the unit, codes rne(v * 1/delta_c)
+// clamped to [-127, 127].  K2 reads V^ as the K-major B operand of a kind::i8 MMA, so the
+// codes are written transposed, [units][d][ldv] with ldv = 64 * ceil(N / 64).
+constexpr int kVRows = 256;  // tokens per k1_v_amax CTA
+
+// Pass 1: channel max |v| of kVRows tokens, merged into vamax (float bits; non-negative
+// floats order like their bit patterns) with one atomicMax per channel and CTA.
 template <typename T, int D>
-cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
+__global__ void __launch_bounds__(kThreads) k1_v_amax(PrepassParams p) {
+    constexpr int CV = D / 8;
+    __shared__ int smax[D];
+    const int tid = threadIdx.x;
+    const int unit = blockIdx.y;
+    const int t0 = blockIdx.x * kVRows;
+    const int rows = min(kVRows, p.n - t0);
+    for (int c = tid; c < D; c += kThreads) smax[c] = 0;
+    __syncthreads();
+    const int cv = tid % CV;
+    float mx[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    bool fin = true;
+    const T* src = static_cast<const T*>(p.v) + (static_cast<size_t>(unit) * p.n + t0) * D + cv * 8;
+    for (int r = tid / CV; r < rows; r += kThreads / CV) {
+        float x[8];
+        load8<T>(src + static_cast<size_t>(r) * D, x);
+        fin &= all_finite8(x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], fabsf(x[i]));
+    }
+    if (!fin) atomicOr(p.status, kStatusNonFinite);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) atomicMax(&smax[cv * 8 + i], __float_as_int(mx[i]));
+    __syncthreads();
+    for (int c = tid; c < D; c += kThreads) atomicMax(&p.vamax[static_cast<size_t>(unit) * D + c], smax[c]);
+}
+
+// Pass 2: 64 tokens x D channels per CTA, quantized and transposed through shared memory.
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads) k1_v_quant(PrepassParams p) {
+    constexpr int CV = D / 8;
+    __shared__ float sinv[D];
+    __shared__ __align__(16) int8_t tile[D][kBlockKV + 16];
+    const int tid = threadIdx.x;
+    const int unit = blockIdx.y;
+    const int t0 = blockIdx.x * kBlockKV;
+    const int rows = min(kBlockKV, p.n - t0);
+    for (int c = tid; c < D; c += kThreads) {
+        const float amax = __int_as_float(__ldcg(&p.vamax[static_cast<size_t>(unit) * D + c]));
+        // quant.hpp:145-151: an all-zero channel takes delta 1 and codes 0.
+        const float delta = amax == 0.0f ? 1.0f : amax / 127.0f;
+        sinv[c] = amax == 0.0f ? 0.0f : 1.0f / delta;
+        if (blockIdx.x == 0) p.vscales[static_cast<size_t>(unit) * D + c] = delta;
+    }
+    __syncthreads();
+    const T* src = static_cast<const T*>(p.v) + (static_cast<size_t>(unit) * p.n + t0) * D;
+    for (int e = tid; e < kBlockKV * CV; e += kThreads) {
+        const int r = e / CV, c8 = (e % CV) * 8;
+        float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (r < rows) load8<T>(src + static_cast<size_t>(r) * D + c8, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float q = rintf(x[i] * sinv[c8 + i]);  // quant.hpp:95-101 (RNE, then clamp)
+            q = fminf(fmaxf(q, -127.0f), 127.0f);
+            tile[c8 + i][r] = static_cast<int8_t>(q);
+        }
+    }
+    __syncthreads();
+    int8_t* dst = p.vcodes + static_cast<size_t>(unit) * D * p.ldv + t0;
+    for (int e = tid; e < D * (kBlockKV / 16); e += kThreads) {
+        const int c = e / (kBlockKV / 16), x16 = (e % (kBlockKV / 16)) * 16;
+        *reinterpret_cast<uint4*>(dst + static_cast<size_t>(c) * p.ldv + x16) =
+            *reinterpret_cast<const uint4*>(&tile[c][x16]);
+    }
+}
+
+template <typename T, int D>
+cudaError_t launch_v(const PrepassParams& p, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(p.vamax, 0, sizeof(int) * static_cast<size_t>(p.units) * D, s);
+    if (e != cudaSuccess) return e;
+    k1_v_amax<T, D><<<dim3((p.n + kVRows - 1) / kVRows, p.units), kThreads, 0, s>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k1_v_quant<T, D><<<dim3((p.n + kBlockKV - 1) / kBlockKV, p.units), kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <typename T, int D>
+cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
     if (std::is_same<T, __half>::value && p.smooth && !p.per_token) {
         const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
@@ -855,6 +941,13 @@ cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     k1_quantize<T, D><<<grid, kQThreads, smem, s>>>(p);
     return cudaGetLastError();
+}
+
+template <typename T, int D>
+cudaError_t launch_typed(const PrepassParams& p, cudaStream_t s) {
+    cudaError_t e = launch_qk<T, D>(p, s);
+    if (e == cudaSuccess && p.vcodes) e = launch_v<T, D>(p, s);
+    return e;
 }
 
 }  // namespace

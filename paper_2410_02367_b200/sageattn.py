@@ -128,17 +128,20 @@ def _raise_for(err: _lib.SabError):
 def _check_b_path(config: KernelConfig, options: SageOptions):
     if config.block_q < 1 or config.block_kv < 1:
         raise ValueError("sage_attention: block sizes must be >= 1")
-    if config.qk_granularity not in (QkGranularity.PerBlock, QkGranularity.PerToken) or \
-            config.pv_path != PvPath.Fp16Acc:
-        raise ValueError("sage_attention: only SAGEAttn-B / SAGEAttn-T (PerBlock or PerToken Q/K, FP16 P~V) "
-                         "run on the B200 path")
+    if config.qk_granularity not in (QkGranularity.PerBlock, QkGranularity.PerToken):
+        raise ValueError("sage_attention: only PerBlock (B, vB) or PerToken (T) Q/K granularity runs on the "
+                         "B200 path")
+    if config.pv_path == PvPath.Int8 and config.qk_granularity != QkGranularity.PerBlock:
+        raise ValueError("sage_attention: SAGEAttn-vT (PerToken Q/K with INT8 P~V) is not built on the B200 path")
     if options.qk_dtype != QuantDtype.Int8:
         raise ValueError("sage_attention: only INT8 Q/K quantization runs on the B200 path")
+    if config.pv_path == PvPath.Int8 and options.pv_dtype != QuantDtype.Int8:
+        raise ValueError("sage_attention: only INT8 P~V quantization runs on the B200 path")
 
 
 def sage_attention(inp: AttentionInput, config: Union[KernelConfig, SageVariant],
                    options: Optional[SageOptions] = None, devices: Optional[Sequence[int]] = None) -> np.ndarray:
-    """SAGEAttn-B / SAGEAttn-T forward on host arrays (B, H, N, d); returns float32 (B, H, N, d).
+    """SAGEAttn-B / -T / -vB forward on host arrays (B, H, N, d); returns float32 (B, H, N, d).
 
     Q/K/V may be float32 (bit-exact prepass for any finite float32 input) or
     float16.  The P~V product always accumulates in FP32 on B200 (the
@@ -161,7 +164,8 @@ def sage_attention(inp: AttentionInput, config: Union[KernelConfig, SageVariant]
         desc = _lib.desc(b, h, n, d, inp.causal, in_dtype=_lib.SAB_F16 if f16 else _lib.SAB_F32,
                          out_dtype=_lib.SAB_F32, block_q=config.block_q, block_kv=config.block_kv,
                          smooth_k=options.smooth_k, check_v=True,
-                         per_token=config.qk_granularity == QkGranularity.PerToken)
+                         per_token=config.qk_granularity == QkGranularity.PerToken,
+                         pv_int8=config.pv_path == PvPath.Int8)
         devs = list(devices) if devices else [0]
         arr = (C.c_int * len(devs))(*devs)
         _lib.check(_lib.load().sab_attention_fwd_host(C.byref(desc), q.ctypes.data, k.ctypes.data, v.ctypes.data,
@@ -214,19 +218,20 @@ def _stream_ptr(stream) -> int:
 
 
 def make_desc(q, causal: bool, out_dtype=None, smooth_k: bool = True, check_v: bool = False,
-              per_token: bool = False) -> _lib.SabDesc:
+              per_token: bool = False, pv_int8: bool = False) -> _lib.SabDesc:
     torch = _torch()
     b, h, n, d = q.shape
     in_dt = _lib.SAB_F16 if q.dtype == torch.float16 else _lib.SAB_F32
     out_dt = _lib.SAB_F32 if out_dtype == torch.float32 else _lib.SAB_F16
     return _lib.desc(b, h, n, d, causal, in_dtype=in_dt, out_dtype=out_dt, smooth_k=smooth_k, check_v=check_v,
-                     per_token=per_token)
+                     per_token=per_token, pv_int8=pv_int8)
 
 
 def prepass_cuda(q, k, v=None, smooth_k: bool = True, ws: Optional[Workspace] = None, stream=None,
-                 per_token: bool = False) -> Workspace:
-    """K1 on CUDA tensors (B,H,N,d) fp16/fp32; returns the workspace holding codes/scales/mean."""
-    desc = make_desc(q, False, smooth_k=smooth_k, per_token=per_token)
+                 per_token: bool = False, pv_int8: bool = False) -> Workspace:
+    """K1 on CUDA tensors (B,H,N,d) fp16/fp32; returns the workspace holding codes/scales/mean
+    (and, with pv_int8, the per-channel V^ of SAGEAttn-vB)."""
+    desc = make_desc(q, False, smooth_k=smooth_k, per_token=per_token, pv_int8=pv_int8)
     ws = ws or Workspace(desc, q.device)
     vptr = v.data_ptr() if v is not None else None
     try:
@@ -250,7 +255,10 @@ def prepass_outputs(ws: Workspace):
                 ws.view("qscales", torch.float32, (units, -(-n // 128))),
                 kscales=ws.view("kscales", torch.float32, (units, npad))[:, :n] if pt else
                 ws.view("kscales", torch.float32, (units, -(-n // 64))),
-                mean=ws.view("mean_k", torch.float32, (units, d)))
+                mean=ws.view("mean_k", torch.float32, (units, d)),
+                **(dict(vcodes=ws.view("vcodes", torch.int8, (units, d, npad))[:, :, :n].transpose(1, 2),
+                        vscales=ws.view("vscales", torch.float32, (units, d)))
+                   if dsc.pv_path == _lib.SAB_PV_PATH_INT8 else {}))
 
 
 def read_status(ws: Workspace, stream=None) -> int:
@@ -260,14 +268,15 @@ def read_status(ws: Workspace, stream=None) -> int:
 
 
 def sage_attention_cuda(q, k, v, causal: bool = False, out=None, out_dtype=None, smooth_k: bool = True,
-                        ws: Optional[Workspace] = None, stream=None, check: bool = True, per_token: bool = False):
+                        ws: Optional[Workspace] = None, stream=None, check: bool = True, per_token: bool = False,
+                        pv_int8: bool = False):
     """K1 + K2 on device-resident CUDA tensors (B,H,N,d); returns O (fp16 by default).
 
     With check=True the stream is synchronised and data-dependent errors raise
     like the reference; with check=False the call stays fully asynchronous."""
     torch = _torch()
     out_dtype = out_dtype or (out.dtype if out is not None else torch.float16)
-    desc = make_desc(q, causal, out_dtype=out_dtype, smooth_k=smooth_k, per_token=per_token)
+    desc = make_desc(q, causal, out_dtype=out_dtype, smooth_k=smooth_k, per_token=per_token, pv_int8=pv_int8)
     if ws is None or ws.nbytes < int(_lib.workspace_layout(desc).total):
         ws = Workspace(desc, q.device)
     ws.desc = desc

@@ -12,6 +12,10 @@ scales (quantize(..., Granularity::per_token())) and O of
 sage_attention(in, SageVariant::T) for both arms:
 
     python tests/golden/make_golden.py --variant-t
+The vb_*.npz fixtures (SAGEAttn-vB) hold the per-channel V^ codes and
+scales (quantize(V, Granularity::per_channel())) and O of
+sage_attention(in, SageVariant::VB):
+    python tests/golden/make_golden.py --variant-vb
 """
 import os
 import sys
@@ -36,6 +40,28 @@ T_CASES = [
     ("t_small", 1, 2, 300, 64, False, "normal"),
     ("t_causal_outlier_d128", 1, 1, 257, 128, True, "outlier"),
 ]
+
+
+VB_CASES = [
+    ("vb_small", 1, 2, 300, 64, False, "normal"),
+    ("vb_causal_outlier_d128", 1, 1, 257, 128, True, "outlier"),
+    ("vb_ragged_causal", 2, 1, 197, 64, True, "normal"),
+]
+
+
+def main_vb():
+    ref = Reference()
+    for name, b, h, n, d, causal, dist in VB_CASES:
+        q, k, v = (x.reshape(b, h, n, d) for x in synth.qkv(b * h, n, d, dtype=np.float16, dist=dist))
+        q32, k32, v32 = (x.astype(np.float32) for x in (q, k, v))
+        vc = np.empty((b * h, n, d), np.int8)
+        vs = np.empty((b * h, d), np.float32)
+        for u in range(b * h):
+            vc[u], vs[u] = ref.quantize_per_channel(v32.reshape(b * h, n, d)[u])
+        o = ref.sage_attention_variant(q32, k32, v32, "VB", causal)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), q=q, k=k, v=v, causal=causal, vcodes=vc, vscales=vs,
+                            o=o)
+        print(name, "written")
 
 
 def main_t():
@@ -71,5 +97,7 @@ def main():
 if __name__ == "__main__":
     if "--variant-t" in sys.argv:
         main_t()
+    elif "--variant-vb" in sys.argv:
+        main_vb()
     else:
         main()

@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sab_abi_version() == 2
+    assert lib.sab_abi_version() == 3
 
 
 def test_desc_validation_mirrors_reference():
@@ -111,8 +111,11 @@ def test_python_mirror_validation_without_gpu():
         sageattn.sage_attention(sageattn.AttentionInput(q, q[:, :, :2], q), sageattn.SageVariant.B)
     with pytest.raises(ValueError, match="block sizes must be >= 1"):
         sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.KernelConfig(block_kv=0))
-    with pytest.raises(ValueError, match="SAGEAttn-B / SAGEAttn-T"):
-        sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.SageVariant.VB)
+    with pytest.raises(ValueError, match="vT"):
+        sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.SageVariant.VT)
+    with pytest.raises(ValueError, match="INT8 P~V"):
+        sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.SageVariant.VB,
+                                sageattn.SageOptions(pv_dtype=sageattn.QuantDtype.FpE4M3))
     assert sageattn.kernel_config_for(sageattn.SageVariant.B) == sageattn.KernelConfig()
     assert sageattn.apply_causal_tiling(0, 2, 128, 64, 1000) == sageattn.TileKind.Skip
 
