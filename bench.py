@@ -200,7 +200,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C2")
-    ap.add_argument("--variant", default="B", choices=["B", "T"],
+    ap.add_argument("--variant", default="B", choices=["B", "T", "VB"],
                     help="B: SAGEAttn-B (per-block Q/K scales, the north-star path); T: SAGEAttn-T (per-token)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -220,6 +220,7 @@ def main():
     n, d, causal = wl["tokens"], wl["head_dim"], wl["causal"]
     total_ops = paper_ops(units_total, n, d, causal)
     per_token = args.variant == "T"
+    pv_int8 = args.variant == "VB"
     config = {"workload": wl["name"], "variant": f"SAGEAttn-{args.variant}", "batch": batch, "heads": wl["heads"], "tokens": n, "head_dim": d,
               "causal": causal, "global_batch": batch,
               "parallelism": (f"head x batch shard over {world} GPUs, no collective" if world > 1 else "single GPU"),
@@ -283,7 +284,7 @@ def main():
         data = "synthetic N(0,1) fp16 (torch.randn, seeded per shard)"
     q, k, v = (h.to(dev) for h in host)
     o = torch.empty_like(q)
-    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16, per_token=per_token)
+    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8)
     ws = sageattn.Workspace(desc, dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -292,7 +293,8 @@ def main():
     import ctypes as C
 
     def step():
-        _lib.check(lib.sab_prepass(C.byref(desc), q.data_ptr(), k.data_ptr(), None, ws.ptr, ws.nbytes, sp))
+        _lib.check(lib.sab_prepass(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr() if pv_int8 else None,
+                                   ws.ptr, ws.nbytes, sp))
         ev[1].record(stream)
         _lib.check(lib.sab_attention(C.byref(desc), ws.ptr, ws.nbytes, v.data_ptr(), o.data_ptr(), sp))
 
@@ -330,12 +332,14 @@ def main():
         e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
         hq, hk, hv = (h.contiguous().pin_memory().numpy() for h in host)
         ho = torch.empty(hq.shape, dtype=torch.float16).pin_memory().numpy()
-        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token)  # warm pool
+        sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token,
+                                     pv_int8=pv_int8)  # warm pool
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token)
+            sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token,
+                                     pv_int8=pv_int8)
         e2e_s = time.perf_counter() - t0
 
     local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s], dtype=torch.float64, device=red_dev)
@@ -369,7 +373,8 @@ def main():
     if rank != 0:
         return
     line = {
-        "metric": METRIC if not per_token else METRIC.replace("SageAttn-B", "SageAttn-T"), "value": value,
+        "metric": METRIC.replace("SageAttn-B", "SageAttn-" + {"B": "B", "T": "T", "VB": "vB"}[args.variant]),
+        "value": value,
         "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int8 QK^T (s32 acc) / fp16 PV (fp32 acc); fp16 Q/K/V/O",
@@ -377,7 +382,8 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * units_total * n * d * 2,
                 "d2h_bytes_per_step": units_total * n * d * 2,
                 "how": "sab_attention_fwd_host on pinned host buffers, wall clock, max over ranks"},
-        "gpu_launches": args.steps * 3,  # k1_mean_partials (+ fused tree top) + k1_quantize + k2_attention
+        # k1_mean_and_q (+ fused tree top) + k1_k_fast + k2_attention; vB adds k1_v_amax + k1_v_quant
+        "gpu_launches": args.steps * (5 if pv_int8 else 3),
         "roofline": {"bound": "tensor", "achieved": k2_ach, "peak": p_mix, "unit": "TFLOP/s",
                      "frac": k2_ach / p_mix, "traffic": traffic, "kernel": "k2_attention",
                      "ms_per_launch": k2_mean_ms,
@@ -398,7 +404,7 @@ def main():
                            "peak": 16.0 * sms * clk * 1e6 / 1e12, "unit": "Texp/s",
                            "frac": exps / (k2_mean_ms * 1e-3) / (16.0 * sms * clk * 1e6),
                            "note": "algorithmic exponentials (one per attended pair); 2/16 run on the FMA pipe"}
-    if world == 1 and not args.no_cpu_baseline and not per_token:
+    if world == 1 and not args.no_cpu_baseline and args.variant == "B":
         threads = args.cpu_threads or os.cpu_count() or 1
         v_cpu, s_cpu, sdesc, used, kind = cpu_reference_sample(wl, threads)
         line["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": used, "kind": kind, "sample": sdesc,

@@ -311,12 +311,12 @@ def qk_int32_tiles_cuda(ws: Workspace, unit: int, q_tile: int, stream=None):
 
 
 def attention_fwd_host(q: np.ndarray, k: np.ndarray, v: np.ndarray, causal: bool, out: np.ndarray,
-                       devices: Sequence[int] = (0,), per_token: bool = False):
+                       devices: Sequence[int] = (0,), per_token: bool = False, pv_int8: bool = False):
     """The C-ABI host-buffer call (sab_attention_fwd_host) on raw fp16/fp32 arrays; `out` receives O."""
     b, h, n, d = q.shape
     in_dt = _lib.SAB_F16 if q.dtype == np.float16 else _lib.SAB_F32
     out_dt = _lib.SAB_F16 if out.dtype == np.float16 else _lib.SAB_F32
-    desc = _lib.desc(b, h, n, d, causal, in_dtype=in_dt, out_dtype=out_dt, per_token=per_token)
+    desc = _lib.desc(b, h, n, d, causal, in_dtype=in_dt, out_dtype=out_dt, per_token=per_token, pv_int8=pv_int8)
     arr = (C.c_int * len(devices))(*devices)
     try:
         _lib.check(_lib.load().sab_attention_fwd_host(C.byref(desc), q.ctypes.data, k.ctypes.data, v.ctypes.data,

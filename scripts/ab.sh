@@ -7,7 +7,7 @@ cp paper_2410_02367_b200/libsageattn_b200.so /tmp/lib_orig.so
 for v in $VARIANTS; do
   cp paper_2410_02367_b200/$v.so paper_2410_02367_b200/libsageattn_b200.so
   for w in ${WORKLOADS:-C2}; do
-    timeout 120 python bench.py --workload $w --steps 20 --warmup 5 --e2e-steps 2 --no-cpu-baseline > /tmp/b.log 2>&1
+    timeout 120 python bench.py $BENCH_ARGS --workload $w --steps 20 --warmup 5 --e2e-steps 2 --no-cpu-baseline > /tmp/b.log 2>&1
     echo "$v $w rc=$? $(python3 -c "
 import json,sys
 l=[x for x in open('/tmp/b.log') if x.startswith('{')]
