@@ -854,11 +854,16 @@ __global__ void __launch_bounds__(kThreads) k1_v_amax(PrepassParams p) {
 }
 
 // Pass 2: 64 tokens x D channels per CTA, quantized and transposed through shared memory.
+// Each work item is 4 consecutive tokens x 8 channels: its 8 channel codes of the 4 tokens
+// are packed into one 32-bit word per channel.  The transposed tile keeps 16 words (64
+// tokens) per channel with the token-quad index XOR-swizzled by the channel octet, so the
+// 16 lanes that share a token quad write 16 different banks.
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) k1_v_quant(PrepassParams p) {
     constexpr int CV = D / 8;
+    constexpr int NQ = kBlockKV / 4;  // token quads per tile
     __shared__ float sinv[D];
-    __shared__ __align__(16) int8_t tile[D][kBlockKV + 16];
+    __shared__ uint32_t tile[D][NQ];
     const int tid = threadIdx.x;
     const int unit = blockIdx.y;
     const int t0 = blockIdx.x * kBlockKV;
@@ -872,23 +877,30 @@ __global__ void __launch_bounds__(kThreads) k1_v_quant(PrepassParams p) {
     }
     __syncthreads();
     const T* src = static_cast<const T*>(p.v) + (static_cast<size_t>(unit) * p.n + t0) * D;
-    for (int e = tid; e < kBlockKV * CV; e += kThreads) {
-        const int r = e / CV, c8 = (e % CV) * 8;
-        float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (r < rows) load8<T>(src + static_cast<size_t>(r) * D + c8, x);
+    for (int e = tid; e < NQ * CV; e += kThreads) {
+        const int cv = e % CV, rq = e / CV;
+        uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            float q = rintf(x[i] * sinv[c8 + i]);  // quant.hpp:95-101 (RNE, then clamp)
-            q = fminf(fmaxf(q, -127.0f), 127.0f);
-            tile[c8 + i][r] = static_cast<int8_t>(q);
+        for (int k = 0; k < 4; ++k) {
+            const int r = 4 * rq + k;
+            float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (r < rows) load8<T>(src + static_cast<size_t>(r) * D + cv * 8, x);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float q = rintf(x[i] * sinv[cv * 8 + i]);  // quant.hpp:95-101 (RNE, then clamp)
+                q = fminf(fmaxf(q, -127.0f), 127.0f);
+                w[i] |= (static_cast<uint32_t>(static_cast<int>(q)) & 0xffu) << (8 * k);
+            }
         }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) tile[cv * 8 + i][rq ^ (cv % NQ)] = w[i];
     }
     __syncthreads();
     int8_t* dst = p.vcodes + static_cast<size_t>(unit) * D * p.ldv + t0;
-    for (int e = tid; e < D * (kBlockKV / 16); e += kThreads) {
-        const int c = e / (kBlockKV / 16), x16 = (e % (kBlockKV / 16)) * 16;
-        *reinterpret_cast<uint4*>(dst + static_cast<size_t>(c) * p.ldv + x16) =
-            *reinterpret_cast<const uint4*>(&tile[c][x16]);
+    for (int e = tid; e < D * (NQ / 4); e += kThreads) {
+        const int c = e / (NQ / 4), q4 = (e % (NQ / 4)) * 4, sw = (c / 8) % NQ;
+        *reinterpret_cast<uint4*>(dst + static_cast<size_t>(c) * p.ldv + 4 * q4) =
+            make_uint4(tile[c][q4 ^ sw], tile[c][(q4 + 1) ^ sw], tile[c][(q4 + 2) ^ sw], tile[c][(q4 + 3) ^ sw]);
     }
 }
 
