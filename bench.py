@@ -200,7 +200,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C2")
-    ap.add_argument("--variant", default="B", choices=["B", "T", "VB"],
+    ap.add_argument("--variant", default="B", choices=["B", "T", "VB", "VT"],
                     help="B: SAGEAttn-B (per-block Q/K scales, the north-star path); T: SAGEAttn-T (per-token)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -219,8 +219,8 @@ def main():
     units_total = batch * wl["heads"]
     n, d, causal = wl["tokens"], wl["head_dim"], wl["causal"]
     total_ops = paper_ops(units_total, n, d, causal)
-    per_token = args.variant == "T"
-    pv_int8 = args.variant == "VB"
+    per_token = args.variant in ("T", "VT")
+    pv_int8 = args.variant in ("VB", "VT")
     config = {"workload": wl["name"], "variant": f"SAGEAttn-{args.variant}", "batch": batch, "heads": wl["heads"], "tokens": n, "head_dim": d,
               "causal": causal, "global_batch": batch,
               "parallelism": (f"head x batch shard over {world} GPUs, no collective" if world > 1 else "single GPU"),
@@ -373,7 +373,7 @@ def main():
     if rank != 0:
         return
     line = {
-        "metric": METRIC.replace("SageAttn-B", "SageAttn-" + {"B": "B", "T": "T", "VB": "vB"}[args.variant]),
+        "metric": METRIC.replace("SageAttn-B", "SageAttn-" + {"B": "B", "T": "T", "VB": "vB", "VT": "vT"}[args.variant]),
         "value": value,
         "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,

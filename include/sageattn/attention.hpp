@@ -21,9 +21,8 @@
 //     P~V accumulator (attention.hpp:84-102, 321, 531-533);
 //   * pure / re-entrant calls (per-call device contexts, attention.hpp:9-12).
 // Differences (documented in INTEGRATION.md):
-//   * only SAGEAttn-B (PerBlock Q/K) and SAGEAttn-T (PerToken Q/K) with Fp16Acc P~V, and
-//     SAGEAttn-vB (PerBlock Q/K with INT8 P~V),
-//     block 128/64 and INT8 run; vT, FP8 dtypes or other block sizes throw
+//   * the four variants B, T (Fp16Acc P~V) and vB, vT (INT8 P~V) with
+//     block 128/64 and INT8 run; FP8 dtypes or other block sizes throw
 //     std::invalid_argument -- there is no CPU fallback;
 //   * head_dim must be 64 or 128;
 //   * P~V accumulates in FP32 on the tensor cores (the reference's
@@ -168,10 +167,7 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
         throw std::invalid_argument("sage_attention: Q, K, V shapes differ");
     if (config.qk_granularity != QkGranularity::PerBlock && config.qk_granularity != QkGranularity::PerToken)
         throw std::invalid_argument(
-            "sage_attention: only PerBlock (B, vB) or PerToken (T) Q/K granularity runs on the B200 path");
-    if (config.pv_path == PvPath::Int8 && config.qk_granularity != QkGranularity::PerBlock)
-        throw std::invalid_argument(
-            "sage_attention: SAGEAttn-vT (PerToken Q/K with INT8 P~V) is not built on the B200 path");
+            "sage_attention: only PerBlock (B, vB) or PerToken (T, vT) Q/K granularity runs on the B200 path");
     if (options.qk_dtype != QuantDtype::Int8)
         throw std::invalid_argument("sage_attention: only INT8 Q/K quantization runs on the B200 path");
     if (config.pv_path == PvPath::Int8 && options.pv_dtype != QuantDtype::Int8)

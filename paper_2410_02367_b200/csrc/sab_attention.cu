@@ -440,6 +440,68 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
     return alpha;
 }
 
+// SAGEAttn-vT: per-token scales (softmax_half_pt's exact pass) with the vB P~ store:
+// scores w*acc per element, exact row max, MUFU exponentials, static-scale INT8 codes.
+template <bool MASK, bool CAUSAL>
+__device__ __forceinline__ float softmax_half_pt_i8(uint32_t (&r)[32], uint32_t ts, int half, float dq,
+                                                    const float* dkp, int kb, int qi, int n, float& m, float& l,
+                                                    bool& rescale) {
+    const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
+    const int lim2 = MASK ? opaque(lim) : lim;
+    float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const float4 dk4 = __ldg(reinterpret_cast<const float4*>(dkp) + g);
+        const f2 w0 = ffma2(f2{dq, dq}, f2{dk4.x, dk4.y}, f2{0.0f, 0.0f});
+        const f2 w1 = ffma2(f2{dq, dq}, f2{dk4.z, dk4.w}, f2{0.0f, 0.0f});
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+            const int c = 4 * g + e;
+            const f2 a = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-kMagicF, -kMagicF});
+            f2 sv = ffma2(a, e == 0 ? w0 : w1, f2{0.0f, 0.0f});
+            if (MASK) {
+                sv.x = (c >= lim) ? -INFINITY : sv.x;
+                sv.y = (c + 1 >= lim) ? -INFINITY : sv.y;
+            }
+            mx4[g & 3] = fmaxf(mx4[g & 3], fmaxf(sv.x, sv.y));
+            r[c] = __float_as_uint(sv.x);
+            r[c + 1] = __float_as_uint(sv.y);
+        }
+    }
+    float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    const float m_new = fmaxf(m, mx);
+    rescale = __any_sync(0xffffffffu, m_new > m);
+    const float alpha = (m_new > m) ? ex2(m - m_new) : 1.0f;
+    m = m_new;
+    const float mref = (m == -INFINITY) ? 0.0f : m;
+    f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t b[4];
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+            const int c = 4 * i + e;
+            const f2 t = fadd2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, f2{-mref, -mref});
+            f2 pp{ex2(t.x), ex2(t.y)};
+            if (MASK) {
+                pp.x = (c >= lim2) ? 0.0f : pp.x;
+                pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
+            }
+            acc[(2 * i + e / 2) & 3] = fadd2(acc[(2 * i + e / 2) & 3], pp);
+            const f2 q = fadd2(ffma2(pp, f2{127.0f, 127.0f}, f2{0.0f, 0.0f}), f2{kMagicF, kMagicF});
+            b[e] = __float_as_uint(q.x);
+            b[e + 1] = __float_as_uint(q.y);
+        }
+        pk[i] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    }
+    tmem_st16x2_8(ts, pk);
+    const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+    l = fmaf(l, alpha, sum.x + sum.y);
+    return alpha;
+}
+
 template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -681,7 +743,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
                 bool rescale;
                 float alpha;
-                if (VI8) {
+                if (VI8 && PT) {
+                    const float* dkp = ksc + kb + 32 * half;
+                    if (need_mask)
+                        alpha = softmax_half_pt_i8<true, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale);
+                    else
+                        alpha = softmax_half_pt_i8<false, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale);
+                } else if (VI8) {
                     if (need_mask)
                         alpha = softmax_half_i8<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale);
                     else
@@ -896,7 +964,8 @@ cudaError_t dispatch_pt(const AttnParams& p, cudaStream_t s) {
 // The INT32 S dump does not read the scales, so it only needs the per-block build.
 template <bool DUMP>
 cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
-    if (!DUMP && p.vcodes) return dispatch_pt<false, false, true>(p, s);  // SAGEAttn-vB
+    if (!DUMP && p.vcodes)  // SAGEAttn-vT / -vB
+        return p.per_token ? dispatch_pt<false, true, true>(p, s) : dispatch_pt<false, false, true>(p, s);
     if (!DUMP && p.per_token) return dispatch_pt<false, true>(p, s);
     return dispatch_pt<DUMP, false>(p, s);
 }

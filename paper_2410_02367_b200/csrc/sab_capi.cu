@@ -225,9 +225,7 @@ int sab_check_desc(const sab_desc* d) {
     if (d->qk_granularity != SAB_QK_PER_BLOCK && d->qk_granularity != SAB_QK_PER_TOKEN)
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: Q/K granularity must be per-block (B) or per-token (T)");
     if (d->pv_path != SAB_PV_PATH_FP16 && d->pv_path != SAB_PV_PATH_INT8)
-        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: P~V path must be FP16 (B/T) or INT8 (vB)");
-    if (d->pv_path == SAB_PV_PATH_INT8 && d->qk_granularity != SAB_QK_PER_BLOCK)
-        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: SAGEAttn-vT (per-token Q/K with INT8 P~V) is not built");
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: P~V path must be FP16 (B/T) or INT8 (vB/vT)");
     if ((d->in_dtype != SAB_F16 && d->in_dtype != SAB_F32) || (d->out_dtype != SAB_F16 && d->out_dtype != SAB_F32))
         return set_error(SAB_ERR_ARGUMENT, "sab_desc: dtype must be SAB_F16 or SAB_F32");
     if (d->pv_accum != SAB_PV_FP32)

@@ -129,10 +129,8 @@ def _check_b_path(config: KernelConfig, options: SageOptions):
     if config.block_q < 1 or config.block_kv < 1:
         raise ValueError("sage_attention: block sizes must be >= 1")
     if config.qk_granularity not in (QkGranularity.PerBlock, QkGranularity.PerToken):
-        raise ValueError("sage_attention: only PerBlock (B, vB) or PerToken (T) Q/K granularity runs on the "
+        raise ValueError("sage_attention: only PerBlock (B, vB) or PerToken (T, vT) Q/K granularity runs on the "
                          "B200 path")
-    if config.pv_path == PvPath.Int8 and config.qk_granularity != QkGranularity.PerBlock:
-        raise ValueError("sage_attention: SAGEAttn-vT (PerToken Q/K with INT8 P~V) is not built on the B200 path")
     if options.qk_dtype != QuantDtype.Int8:
         raise ValueError("sage_attention: only INT8 Q/K quantization runs on the B200 path")
     if config.pv_path == PvPath.Int8 and options.pv_dtype != QuantDtype.Int8:
@@ -141,7 +139,7 @@ def _check_b_path(config: KernelConfig, options: SageOptions):
 
 def sage_attention(inp: AttentionInput, config: Union[KernelConfig, SageVariant],
                    options: Optional[SageOptions] = None, devices: Optional[Sequence[int]] = None) -> np.ndarray:
-    """SAGEAttn-B / -T / -vB forward on host arrays (B, H, N, d); returns float32 (B, H, N, d).
+    """SAGEAttn-B / -T / -vB / -vT forward on host arrays (B, H, N, d); returns float32 (B, H, N, d).
 
     Q/K/V may be float32 (bit-exact prepass for any finite float32 input) or
     float16.  The P~V product always accumulates in FP32 on B200 (the

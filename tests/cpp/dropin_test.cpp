@@ -52,10 +52,13 @@ int main(int argc, char** argv) {
     const sageattn::Tensor4f out_t = sageattn::sage_attention(in, sageattn::SageVariant::T);
     std::ofstream(std::string(argv[9]) + ".t", std::ios::binary)
         .write(reinterpret_cast<const char*>(out_t.data.data()), std::streamsize(out_t.size() * sizeof(float)));
-    // SAGEAttn-vB (INT8 P~V).
+    // SAGEAttn-vB / -vT (INT8 P~V).
     const sageattn::Tensor4f out_vb = sageattn::sage_attention(in, sageattn::SageVariant::VB);
     std::ofstream(std::string(argv[9]) + ".vb", std::ios::binary)
         .write(reinterpret_cast<const char*>(out_vb.data.data()), std::streamsize(out_vb.size() * sizeof(float)));
+    const sageattn::Tensor4f out_vt = sageattn::sage_attention(in, sageattn::SageVariant::VT);
+    std::ofstream(std::string(argv[9]) + ".vt", std::ios::binary)
+        .write(reinterpret_cast<const char*>(out_vt.data.data()), std::streamsize(out_vt.size() * sizeof(float)));
     std::printf("MACS %llu %llu\n", (unsigned long long)diag.s_stage_macs, (unsigned long long)diag.pv_stage_macs);
 
     bool ok = true;
@@ -70,8 +73,10 @@ int main(int argc, char** argv) {
     nan_in.k.data[nan_in.k.size() / 2] = std::nanf("");
     ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(nan_in, sageattn::SageVariant::B); },
                                         "non-finite input");
-    ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(in, sageattn::SageVariant::VT); },
-                                        "SAGEAttn-vT");
+    sageattn::SageOptions fp8;
+    fp8.qk_dtype = sageattn::QuantDtype::FpE4M3;
+    ok &= throws<std::invalid_argument>([&] { sageattn::sage_attention(in, sageattn::SageVariant::B, fp8); },
+                                        "only INT8 Q/K");
     ok &= sageattn::apply_causal_tiling(0, 2, 128, 64, 1000) == sageattn::TileKind::Skip;
     std::printf(ok ? "ERRORS OK\n" : "ERRORS FAILED\n");
     return ok ? 0 : 1;

@@ -14,7 +14,7 @@ sage_attention(in, SageVariant::T) for both arms:
     python tests/golden/make_golden.py --variant-t
 The vb_*.npz fixtures (SAGEAttn-vB) hold the per-channel V^ codes and
 scales (quantize(V, Granularity::per_channel())) and O of
-sage_attention(in, SageVariant::VB):
+sage_attention(in, SageVariant::VB) and of SageVariant::VT (o_vt):
     python tests/golden/make_golden.py --variant-vb
 """
 import os
@@ -59,8 +59,9 @@ def main_vb():
         for u in range(b * h):
             vc[u], vs[u] = ref.quantize_per_channel(v32.reshape(b * h, n, d)[u])
         o = ref.sage_attention_variant(q32, k32, v32, "VB", causal)
+        o_vt = ref.sage_attention_variant(q32, k32, v32, "VT", causal)
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), q=q, k=k, v=v, causal=causal, vcodes=vc, vscales=vs,
-                            o=o)
+                            o=o, o_vt=o_vt)
         print(name, "written")
 
 

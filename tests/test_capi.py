@@ -111,8 +111,6 @@ def test_python_mirror_validation_without_gpu():
         sageattn.sage_attention(sageattn.AttentionInput(q, q[:, :, :2], q), sageattn.SageVariant.B)
     with pytest.raises(ValueError, match="block sizes must be >= 1"):
         sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.KernelConfig(block_kv=0))
-    with pytest.raises(ValueError, match="vT"):
-        sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.SageVariant.VT)
     with pytest.raises(ValueError, match="INT8 P~V"):
         sageattn.sage_attention(sageattn.AttentionInput(q, q, q), sageattn.SageVariant.VB,
                                 sageattn.SageOptions(pv_dtype=sageattn.QuantDtype.FpE4M3))

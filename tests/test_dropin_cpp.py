@@ -57,3 +57,6 @@ def test_dropin_runs_on_b200(tmp_path, cuda, oracle, shape, causal):
     o_vb = np.fromfile(str(out) + ".vb", np.float32).reshape(b * h, n, d)
     ref_vb, _ = oracle.sage(q, k, v, causal, pv_int8=True)
     assert cosine_sim(o_vb, ref_vb) >= 0.9999 and relative_l1(o_vb, ref_vb) <= 2e-3
+    o_vt = np.fromfile(str(out) + ".vt", np.float32).reshape(b * h, n, d)
+    ref_vt, _ = oracle.sage(q, k, v, causal, pv_int8=True, per_token=True)
+    assert cosine_sim(o_vt, ref_vt) >= 0.9999 and relative_l1(o_vt, ref_vt) <= 2e-3

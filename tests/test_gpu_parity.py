@@ -176,8 +176,6 @@ def test_error_paths(cuda):
     badv[0, 0, 7, 1] = np.nan
     with pytest.raises(ValueError, match="non-finite input"):
         sage_attention(AttentionInput(q, k, badv), SageVariant.B)
-    with pytest.raises(ValueError):  # T and vB run on the B200 path (test_gpu_variant_{t,vb}.py)
-        sage_attention(AttentionInput(q, k, v), SageVariant.VT)
     with pytest.raises(ValueError):
         sage_attention(AttentionInput(q, k, v), SageVariant.B, SageOptions(qk_dtype=QuantDtype.FpE4M3))
 

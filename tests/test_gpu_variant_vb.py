@@ -1,5 +1,5 @@
-"""GPU parity of SAGEAttn-vB: static-scale INT8 P~, per-channel INT8 V,
-INT32 P~V products on tcgen05 kind::i8, in the same K1/K2.
+"""GPU parity of SAGEAttn-vB / -vT: static-scale INT8 P~, per-channel INT8 V,
+INT32 P~V products on tcgen05 kind::i8, in the same K1/K2 (vT: with per-token Q/K scales).
 
 Bit-exact: K1's per-channel V^ codes and scales (quantize(V, per_channel), quant.hpp:128-173)
 against the oracle, which tests/test_oracle.py pins to the compiled reference
@@ -73,8 +73,9 @@ VB_CASES = [
 ]
 
 
+@pytest.mark.parametrize("per_token", [False, True], ids=["vB", "vT"])
 @pytest.mark.parametrize("shape,causal,dist", VB_CASES)
-def test_attention_vb_within_tolerance(cuda, oracle, shape, causal, dist):
+def test_attention_vb_within_tolerance(cuda, oracle, shape, causal, dist, per_token):
     import torch
 
     from paper_2410_02367_b200 import sage_attention_cuda
@@ -82,16 +83,16 @@ def test_attention_vb_within_tolerance(cuda, oracle, shape, causal, dist):
     b, h, n, d = shape
     q, k, v = _qkv(b, h, n, d, dist=dist)
     qd, kd, vd = _dev([q, k, v], torch.float16, cuda)
-    o = sage_attention_cuda(qd, kd, vd, causal=causal, out_dtype=torch.float32, pv_int8=True)
+    o = sage_attention_cuda(qd, kd, vd, causal=causal, out_dtype=torch.float32, pv_int8=True, per_token=per_token)
     o = o.cpu().numpy().reshape(-1, n, d)
     f16 = [x.reshape(-1, n, d).astype(np.float16).astype(np.float32) for x in (q, k, v)]
-    ref, _ = oracle.sage(*f16, causal, pv_int8=True)
+    ref, _ = oracle.sage(*f16, causal, pv_int8=True, per_token=per_token)
     cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
     assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)
 
 
 def test_dropin_variant_vb(cuda, oracle):
-    """sage_attention(in, SageVariant::VB) through the host C ABI, fp32 inputs (V^ from fp32 V)."""
+    """sage_attention(in, SageVariant::VB / VT) through the host C ABI, fp32 inputs (V^ from fp32 V)."""
     from paper_2410_02367_b200.sageattn import AttentionInput, SageVariant, sage_attention
 
     b, h, n, d = 1, 2, 333, 64
@@ -101,8 +102,11 @@ def test_dropin_variant_vb(cuda, oracle):
     ref, _ = oracle.sage(q.reshape(-1, n, d), k.reshape(-1, n, d), v.reshape(-1, n, d), True, pv_int8=True)
     cs, rl = cosine_sim(o.reshape(-1, n, d), ref), relative_l1(o.reshape(-1, n, d), ref)
     assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)
-    with pytest.raises(ValueError):
-        sage_attention(AttentionInput(q, k, v), SageVariant.VT)
+    o = sage_attention(AttentionInput(q, k, v, causal=True), SageVariant.VT)
+    ref, _ = oracle.sage(q.reshape(-1, n, d), k.reshape(-1, n, d), v.reshape(-1, n, d), True, pv_int8=True,
+                         per_token=True)
+    cs, rl = cosine_sim(o.reshape(-1, n, d), ref), relative_l1(o.reshape(-1, n, d), ref)
+    assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)
     v[0, 1, 7, 3] = np.inf
     with pytest.raises(ValueError, match="non-finite"):
         sage_attention(AttentionInput(q, k, v), SageVariant.VB)
@@ -129,3 +133,8 @@ def test_vb_against_reference_fixtures(cuda, path):
     o, ref = o.cpu().numpy().reshape(-1, n, d), g["o"].reshape(-1, n, d)
     cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
     assert cs >= COS_MIN and rl <= REL_L1_MAX, (cs, rl)
+    o = sage_attention_cuda(qd, kd, vd, causal=bool(g["causal"]), out_dtype=torch.float32, pv_int8=True,
+                            per_token=True)
+    o, ref = o.cpu().numpy().reshape(-1, n, d), g["o_vt"].reshape(-1, n, d)
+    cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
+    assert cs >= COS_MIN and rl <= REL_L1_MAX, ("vT", cs, rl)
