@@ -2,7 +2,8 @@
 
 The compute path is libsageattn_b200.so behind the C ABI in
 include/sageattn_b200.h; this package only mirrors the reference interface
-(sageattn.py) and binds the library (_lib.py).
+(sageattn.py), binds the library (_lib.py) and adds the host-side adaptive
+kernel selection of SPEC.md's metrics-adaptive module (calibrate.py).
 """
 from .sageattn import (  # noqa: F401
     AttentionInput, KernelConfig, PvPath, QkGranularity, QuantDtype, SageDiagnostics, SageOptions, SageVariant,
