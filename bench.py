@@ -192,6 +192,22 @@ def cpu_reference_sample(wl, threads: int, target_s: float = 12.0):
     return ops / dt / 1e12, dt, desc, len(lists), kind
 
 
+def overlap_groups(spec: str, count: int, n: int, d: int) -> list:
+    """Unit-group sizes of the overlapped step ('off' -> one group)."""
+    if spec == "off" or count < 2:
+        return [count]
+    if spec == "auto":
+        # Measured slower than one launch each on C2 and C3 (profiles/r01_experiments.md:
+        # K2's 576-thread CTAs leave no room for K1 CTAs until its last wave drains).
+        return [count]
+    sizes = [int(x) for x in spec.split(",") if x]
+    if len(sizes) == 1:
+        sizes.append(count - sizes[0])
+    if sum(sizes) != count or min(sizes) < 1:
+        raise SystemExit(f"--groups {spec}: sizes must be positive and sum to the shard's {count} units")
+    return sizes
+
+
 # ----------------------------------------------------------------------------- main
 
 def main():
@@ -204,6 +220,9 @@ def main():
                     help="B: SAGEAttn-B (per-block Q/K scales, the north-star path); T: SAGEAttn-T (per-token)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--groups", default="auto",
+                    help="K1/K2 overlap: comma list of unit-group sizes (e.g. '8,24'), 'auto', or 'off'. "
+                         "Group g's K2 runs on its own stream while group g+1's K1 runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=None)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -307,6 +326,51 @@ def main():
     torch.cuda.synchronize()
     _lib.check(sageattn.read_status(ws))
 
+    # Overlapped step: the shard's units in groups, each group with its own workspace
+    # and stream.  K1(g) starts when K1(g-1) has finished (so earlier groups get HBM
+    # first); K2(g) follows K1(g) on group g's stream, so K1 of later groups fills the
+    # SMs K2 of earlier groups leaves idle in its last wave.  Units are independent
+    # (SURVEY F2), so the groups compute exactly what the one-launch step computes.
+    groups = overlap_groups(args.groups, count, n, d)
+    if len(groups) > 1:
+        gsteps, g0 = [], 0
+        for gi, gc in enumerate(groups):
+            sl = slice(g0, g0 + gc)
+            gq, gk, gv, go = (t[:, sl] for t in (q, k, v, o))
+            gdesc = sageattn.make_desc(gq, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8)
+            gsteps.append((gdesc, sageattn.Workspace(gdesc, dev), gq, gk, gv, go,
+                           stream if gi == 0 else torch.cuda.Stream(dev), torch.cuda.Event()))
+            g0 += gc
+        join = [torch.cuda.Event() for _ in groups]
+        fork = torch.cuda.Event()
+
+        def step_overlap():
+            fork.record(stream)
+            prev = fork
+            for gi, (gdesc, gws, gq, gk, gv, go, gs, k1_done) in enumerate(gsteps):
+                gs.wait_event(prev)
+                gp = gs.cuda_stream
+                _lib.check(lib.sab_prepass(C.byref(gdesc), gq.data_ptr(), gk.data_ptr(),
+                                           gv.data_ptr() if pv_int8 else None, gws.ptr, gws.nbytes, gp))
+                k1_done.record(gs)
+                prev = k1_done
+                _lib.check(lib.sab_attention(C.byref(gdesc), gws.ptr, gws.nbytes, gv.data_ptr(), go.data_ptr(), gp))
+                join[gi].record(gs)
+            for e in join[1:]:
+                stream.wait_event(e)
+
+        step()
+        o_serial = o.clone()
+        o.zero_()
+        for _ in range(args.warmup):
+            flush.fill_(1)
+            step_overlap()
+        torch.cuda.synchronize()
+        if not torch.equal(o, o_serial):
+            raise SystemExit("overlapped step differs from the one-launch step")
+        for g in gsteps:
+            _lib.check(sageattn.read_status(g[1]))
+
     sampler = ClockSampler(dev.index)
     t_step, t_k1, t_k2 = [], [], []
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
@@ -325,6 +389,19 @@ def main():
             t_step.append(ev[0].elapsed_time(ev[2]))
             t_k1.append(ev[0].elapsed_time(ev[1]))
             t_k2.append(ev[1].elapsed_time(ev[2]))
+        t_serial = list(t_step)
+        if len(groups) > 1:
+            # The headline step is the overlapped one; the serial pass above still
+            # provides the per-kernel (K1, K2) times for the rooflines.
+            t_step = []
+            for i in range(args.steps):
+                flush.fill_(2)
+                ev = evs[i]
+                ev[0].record(stream)
+                step_overlap()
+                ev[2].record(stream)
+            torch.cuda.synchronize()
+            t_step = [ev[0].elapsed_time(ev[2]) for ev in evs]
         if dist:
             dist.barrier()
 
@@ -342,10 +419,11 @@ def main():
                                      pv_int8=pv_int8)
         e2e_s = time.perf_counter() - t0
 
-    local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s], dtype=torch.float64, device=red_dev)
+    local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s, sum(t_serial)], dtype=torch.float64,
+                         device=red_dev)
     if dist:
         dist.all_reduce(local, op=dist.ReduceOp.MAX)
-    tot_ms, k1_ms, k2_ms, e2e_max = local.tolist()
+    tot_ms, k1_ms, k2_ms, e2e_max, serial_ms = local.tolist()
     ms_per_step = tot_ms / args.steps
     value = total_ops / (ms_per_step * 1e-3) / 1e12
     e2e_value = total_ops * e2e_steps / e2e_max / 1e12
@@ -383,7 +461,7 @@ def main():
                 "d2h_bytes_per_step": units_total * n * d * 2,
                 "how": "sab_attention_fwd_host on pinned host buffers, wall clock, max over ranks"},
         # k1_mean_and_q (+ fused tree top) + k1_k_fast + k2_attention; vB adds k1_v_amax + k1_v_quant
-        "gpu_launches": args.steps * (5 if pv_int8 else 3),
+        "gpu_launches": args.steps * (5 if pv_int8 else 3) * len(groups),
         "roofline": {"bound": "tensor", "achieved": k2_ach, "peak": p_mix, "unit": "TFLOP/s",
                      "frac": k2_ach / p_mix, "traffic": traffic, "kernel": "k2_attention",
                      "ms_per_launch": k2_mean_ms,
@@ -394,6 +472,9 @@ def main():
                         "unit": "GB/s", "frac": k1_alg / (k1_mean_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                         "ms_per_step": k1_mean_ms, "alg_bytes": k1_alg, "min_dram_bytes_with_k_reread": k1_bytes},
         "clocks": sampler.summary(),
+        "step_schedule": {"groups": groups, "ms_per_step_serial": serial_ms / args.steps,
+                          "note": "K1(g+1) overlaps K2(g) on per-group streams" if len(groups) > 1
+                          else "K1 then K2, one launch each"},
     }
     # Second bound of K2: one exp2 per attended (query, key) pair on MUFU (16 lanes/clk/SM,
     # profiles/r01_micro_mufu.txt); 2 of every 16 run on the FMA pipe instead.

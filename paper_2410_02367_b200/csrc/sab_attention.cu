@@ -579,6 +579,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
+    // Everything above is independent of K1; Q^/K^/scales/V are read only below.
+    griddep_wait();
 
     if (warp == 16) {
         // ------------------------------------------------------------ TMA producer
@@ -941,8 +943,7 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     cudaMemcpyToSymbolAsync(g_trace, &h_trace_ptr, sizeof(h_trace_ptr), 0, cudaMemcpyHostToDevice, s);
     cudaMemcpyToSymbolAsync(g_trace_cta, &h_trace_cta, sizeof(int), 0, cudaMemcpyHostToDevice, s);
 #endif
-    kern<<<grid, kThreads, C::kSmemBytes, s>>>(tq, tk, tv, pp);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, tq, tk, tv, pp);
 }
 
 template <bool DUMP, bool PT, bool VI8 = false>

@@ -3,6 +3,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/sageattn_b200.h"
@@ -72,5 +74,32 @@ struct AttnParams {
 
 cudaError_t launch_attention(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_qk_dump(const AttnParams& p, cudaStream_t s);
+
+// PDL between K1a -> K1b -> K2 on the fast path (SAB_PDL=0 turns it off).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SAB_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Launches `kern` on `s`, with the programmatic-stream-serialization attribute when
+// PDL is enabled (the kernel must call griddep_wait before reading its producer's output).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace sab

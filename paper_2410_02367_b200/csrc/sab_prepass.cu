@@ -716,6 +716,7 @@ __device__ __forceinline__ void q_chunk_fast(const PrepassParams& p, int unit, i
 template <int D, int G>
 __global__ void __launch_bounds__(kQThreads, SAB_K1_MINB) k1_mean_and_q(PrepassParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
+    griddep_launch_dependents();  // k1_k_fast may be scheduled behind this grid's last wave
     if (static_cast<int>(blockIdx.x) < p.n_partials) mean_partial<__half, D, G>(p, blockIdx.y, blockIdx.x);
     else q_chunk_fast<D>(p, blockIdx.y, blockIdx.x - p.n_partials, smem);
 }
@@ -742,6 +743,10 @@ __global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
         bulk_load(smem_u32(smem), static_cast<const __half*>(p.k) + ubase + static_cast<size_t>(r0) * D, bytes,
                   smem_u32(&bar));
     }
+    // K is an input: its load is in flight before mean(K) (k1_mean_and_q's output) is
+    // awaited.  Every CTA waits, so this grid never completes before its producer.
+    griddep_wait();
+    griddep_launch_dependents();  // K2 may be scheduled behind this grid's last wave
     if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
     __syncthreads();
     mbar_wait(smem_u32(&bar), 0);
@@ -933,8 +938,7 @@ cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         e = cudaFuncSetAttribute(k1_k_fast<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        k1_k_fast<D><<<dim3(ntq, p.units), kQThreads, smem, s>>>(p);
-        return cudaGetLastError();
+        return launch_pdl(k1_k_fast<D>, dim3(ntq, p.units), dim3(kQThreads), smem, s, p);
     }
     if (p.smooth) {
         const dim3 grid(p.n_partials, p.units);
