@@ -37,3 +37,16 @@ def test_paper_ops_and_workloads():
     w = bench.workload("C4-128-16384-nc")
     assert (w["batch"], w["heads"], w["tokens"], w["head_dim"], w["causal"]) == (4, 32, 16384, 128, False)
     assert bench.workload("C5")["tokens"] == 131072
+
+
+def test_overlap_groups():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert bench.overlap_groups("auto", 32, 8192, 128) == [32]  # measured: one launch each is fastest
+    assert bench.overlap_groups("off", 60, 17776, 64) == [60]
+    assert bench.overlap_groups("8", 32, 8192, 128) == [8, 24]
+    assert bench.overlap_groups("4,8,20", 32, 8192, 128) == [4, 8, 20]
+    assert bench.overlap_groups("8,24", 1, 8192, 128) == [1]
+    with pytest.raises(SystemExit):
+        bench.overlap_groups("8,8", 32, 8192, 128)
