@@ -1,84 +1,55 @@
-// sageattn/attention.hpp -- B200 drop-in for the reference's SAGEAttn-B / -T entry point.
+// sageattn/attention.hpp -- B200 drop-in for the reference's attention entry points.
 //
 // Source-compatible replacement for /root/reference/proj/include/sageattn/
-// attention.hpp as far as the SAGEAttn-B hot path goes: an application that
-// calls
-//     sageattn::sage_attention(const AttentionInput&, SageVariant::B | SageVariant::T, const SageOptions&)
+// attention.hpp: an application that calls
+//     sageattn::sage_attention(const AttentionInput&, SageVariant, const SageOptions&)
 //     sageattn::sage_attention(const AttentionInput&, const KernelConfig&, const SageOptions&)
 // (attention.hpp:318-319, 547-550) switches to the B200 path by putting
 // <repo>/include first on its include path and linking
-// paper_2410_02367_b200/libsageattn_b200.so.  Everything below is a thin
-// header over the C ABI in sageattn_b200.h; the arithmetic runs in the CUDA
-// kernels (K1 prepass + K2 tcgen05 attention, K3 head x batch sharding).
+// paper_2410_02367_b200/libsageattn_b200.so.  sage_attention is a thin header
+// over the C ABI in sageattn_b200.h; the arithmetic runs in the CUDA kernels
+// (K1 prepass + K2 tcgen05 attention, K3 head x batch sharding over every
+// visible sm_100 device).
 //
 // Kept from the reference contract:
-//   * the types AttentionInput, KernelConfig, QkGranularity, PvPath, SageVariant,
-//     SageOptions, SageDiagnostics, QuantDtype, Tensor4f / Tensor4d, TileKind with
-//     the same members and layouts (tensor.hpp:58-107 (B,H,N,d) row-major);
-//   * kernel_config_for, apply_causal_tiling;
+//   * the carriers Matrix / MatView / Tensor4 (tensor.hpp), QuantDtype (quant.hpp)
+//     and AttentionInput, KernelConfig, QkGranularity, PvPath, SageVariant,
+//     SageOptions, SageDiagnostics, TileKind with the same members and layouts;
+//   * kernel_config_for, apply_causal_tiling, naive_attention, flash_attention_fp;
 //   * exceptions and messages: std::invalid_argument for bad block sizes,
 //     shape mismatch and non-finite input, std::overflow_error for a non-finite
 //     P~V accumulator (attention.hpp:84-102, 321, 531-533);
-//   * pure / re-entrant calls (per-call device contexts, attention.hpp:9-12).
-// Differences (documented in INTEGRATION.md):
-//   * the four variants B, T (Fp16Acc P~V) and vB, vT (INT8 P~V) with
-//     block 128/64 and INT8 run; FP8 dtypes or other block sizes throw
-//     std::invalid_argument -- there is no CPU fallback;
+//   * pure / re-entrant calls (per-call device contexts, attention.hpp:9-12);
+//   * SageDiagnostics: the MAC counters (404, 445) and, on the INT8 P~V path,
+//     the static-scale P~ mismatch counters (479-488), counted on the GPU.
+// Differences:
+//   * the four variants B, T (Fp16Acc P~V) and vB, vT (INT8 P~V) with block
+//     128/64 and INT8 Q/K run; FP8 dtypes, PerTensor scales or other block sizes
+//     throw std::invalid_argument -- there is no CPU fallback for sage_attention;
 //   * head_dim must be 64 or 128;
 //   * P~V accumulates in FP32 on the tensor cores (the reference's
 //     pv_fp32_accumulator arm) whatever pv_fp32_accumulator says; Q^/K^ codes,
 //     scales and mean(K) are bit-identical to the reference.
+// naive_attention (the binary64 exact oracle, attention.hpp:107-149) and
+// flash_attention_fp (the binary32 tiled baseline, 169-252) are not on the
+// SageAttn path; they stay host functions here so programs that compare
+// against them keep compiling and behaving as before.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
-#include <span>
+#include <limits>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "../sageattn_b200.h"
+#include "quant.hpp"
+#include "tensor.hpp"
 
 namespace sageattn {
-
-enum class QuantDtype : uint8_t { Int8, FpE4M3, FpE5M2 };
-
-// Dense (batch, heads, tokens, head_dim) container; each (b, h) slice is a
-// contiguous tokens x head_dim block.
-template <typename T>
-struct Tensor4 {
-    int batch = 0, heads = 0, tokens = 0, head_dim = 0;
-    std::vector<T> data;
-
-    Tensor4() = default;
-    Tensor4(int b, int h, int n, int d, T fill = T{}) : batch(b), heads(h), tokens(n), head_dim(d) {
-        if (b < 1 || h < 1 || n < 1 || d < 1) throw std::invalid_argument("tensor dimensions must be positive");
-        data.assign(size_t(b) * size_t(h) * size_t(n) * size_t(d), fill);
-    }
-    size_t size() const { return data.size(); }
-    size_t offset(int b, int h, int t, int c) const {
-        return ((size_t(b) * size_t(heads) + size_t(h)) * size_t(tokens) + size_t(t)) * size_t(head_dim) + size_t(c);
-    }
-    T& at(int b, int h, int t, int c) { return data[offset(b, h, t, c)]; }
-    const T& at(int b, int h, int t, int c) const { return data[offset(b, h, t, c)]; }
-    T* slice_ptr(int b, int h) { return data.data() + offset(b, h, 0, 0); }
-    const T* slice_ptr(int b, int h) const { return data.data() + offset(b, h, 0, 0); }
-    std::span<const T> slice_span(int b, int h) const {
-        return {slice_ptr(b, h), size_t(tokens) * size_t(head_dim)};
-    }
-    bool same_shape(const Tensor4& o) const {
-        return batch == o.batch && heads == o.heads && tokens == o.tokens && head_dim == o.head_dim;
-    }
-    bool all_finite() const {
-        for (const T& v : data)
-            if (!std::isfinite(static_cast<double>(v))) return false;
-        return true;
-    }
-};
-
-using Tensor4f = Tensor4<float>;
-using Tensor4d = Tensor4<double>;
 
 struct AttentionInput {
     Tensor4f q;
@@ -127,8 +98,8 @@ enum class TileKind : uint8_t { Full, Diagonal, Skip };
 inline TileKind apply_causal_tiling(int i, int j, int block_q, int block_kv, int n_tokens) {
     if (block_q < 1 || block_kv < 1) throw std::invalid_argument("block sizes must be >= 1");
     const int r0 = i * block_q, c0 = j * block_kv;
-    const int r1 = (r0 + block_q < n_tokens ? r0 + block_q : n_tokens) - 1;
-    const int c1 = (c0 + block_kv < n_tokens ? c0 + block_kv : n_tokens) - 1;
+    const int r1 = std::min(r0 + block_q, n_tokens) - 1;
+    const int c1 = std::min(c0 + block_kv, n_tokens) - 1;
     if (r0 < 0 || r0 > r1 || c0 < 0 || c0 > c1 || r1 >= n_tokens || c1 >= n_tokens)
         throw std::invalid_argument("tile indices out of range");
     if (c0 > r1) return TileKind::Skip;
@@ -151,10 +122,29 @@ inline void throw_status(int status) {
     }
 }
 
-// Devices used by the host-buffer path (K3 sharding); 0 = all visible.
+// Devices the host-buffer path (K3) shards over: 0 = every visible sm_100 device,
+// n > 0 = the first n of them.
 inline int& device_count_override() {
     static int n = 1;
     return n;
+}
+
+// The sm_100 ordinals a call uses (never a device of another architecture).
+inline std::vector<int> devices_for_call() {
+    int n = 0;
+    throw_status(sab_device_ordinals(nullptr, 0, &n));
+    std::vector<int> ids(size_t(std::max(n, 1)), 0);
+    if (n > 0) throw_status(sab_device_ordinals(ids.data(), n, &n));
+    const int want = device_count_override();
+    if (want > 0 && want < int(ids.size())) ids.resize(size_t(want));
+    return ids;
+}
+
+inline void validate_input(const AttentionInput& in, const char* what) {
+    if (!in.q.same_shape(in.k) || !in.q.same_shape(in.v))
+        throw std::invalid_argument(std::string(what) + ": Q, K, V shapes differ");
+    if (!in.q.all_finite() || !in.k.all_finite() || !in.v.all_finite())
+        throw std::invalid_argument(std::string(what) + ": non-finite input");
 }
 
 }  // namespace b200
@@ -183,22 +173,127 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
     d.check_v = 1;  // validate_input scans V too (attention.hpp:101)
     d.qk_granularity = config.qk_granularity == QkGranularity::PerToken ? SAB_QK_PER_TOKEN : SAB_QK_PER_BLOCK;
     d.pv_path = config.pv_path == PvPath::Int8 ? SAB_PV_PATH_INT8 : SAB_PV_PATH_FP16;
+    // attention.hpp:479: the static-scale counters exist only on the INT8 P~V path.
+    SageDiagnostics* diag = options.diagnostics;
+    d.measure_static_scale = (diag && diag->measure_static_scale && d.pv_path == SAB_PV_PATH_INT8) ? 1 : 0;
     Tensor4f out(in.q.batch, in.q.heads, in.q.tokens, in.q.head_dim);
-    int n_dev = b200::device_count_override();
-    if (n_dev <= 0) sab_device_count(&n_dev);
-    b200::throw_status(sab_attention_fwd_host(&d, in.q.data.data(), in.k.data.data(), in.v.data.data(),
-                                              out.data.data(), nullptr, n_dev > 0 ? n_dev : 1));
-    if (options.diagnostics) {
+    const std::vector<int> devs = b200::devices_for_call();
+    uint64_t counts[3] = {0, 0, 0};
+    b200::throw_status(sab_attention_fwd_host_diag(&d, in.q.data.data(), in.k.data.data(), in.v.data.data(),
+                                                   out.data.data(), devs.data(), int(devs.size()), counts));
+    if (diag) {
         uint64_t s = 0, p = 0;
         b200::throw_status(sab_diagnostics(&d, &s, &p));
-        options.diagnostics->s_stage_macs += s;
-        options.diagnostics->pv_stage_macs += p;
+        diag->s_stage_macs += s;
+        diag->pv_stage_macs += p;
+        if (d.measure_static_scale) {
+            diag->static_scale_elements += counts[0];
+            diag->static_scale_first_block_mismatches += counts[1];
+            diag->static_scale_later_block_mismatches += counts[2];
+        }
     }
     return out;
 }
 
 inline Tensor4f sage_attention(const AttentionInput& in, SageVariant variant, const SageOptions& options = {}) {
     return sage_attention(in, kernel_config_for(variant), options);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Host functions outside the SageAttn path, kept so reference-API programs still build.
+
+// Exact attention in binary64 (attention.hpp:107-149): scores Q K^T / sqrt(d), causal
+// mask j > i, softmax and P V all accumulated in double.
+inline Tensor4d naive_attention(const AttentionInput& in) {
+    b200::validate_input(in, "naive_attention");
+    const int n = in.q.tokens, d = in.q.head_dim;
+    const double scale = 1.0 / std::sqrt(double(d));
+    Tensor4d out(in.q.batch, in.q.heads, n, d);
+    std::vector<double> w(size_t(n), 0.0);
+    for (int b = 0; b < in.q.batch; ++b)
+        for (int h = 0; h < in.q.heads; ++h) {
+            const MatView<float> Q = in.q.slice(b, h), K = in.k.slice(b, h), V = in.v.slice(b, h);
+            double* O = out.slice_ptr(b, h);
+            for (int t = 0; t < n; ++t) {
+                const int keys = in.causal ? t + 1 : n;
+                double mx = -std::numeric_limits<double>::infinity();
+                for (int j = 0; j < keys; ++j) {
+                    double dot = 0.0;
+                    for (int c = 0; c < d; ++c) dot += double(Q(t, c)) * double(K(j, c));
+                    w[size_t(j)] = dot * scale;
+                    mx = std::max(mx, w[size_t(j)]);
+                }
+                double sum = 0.0;
+                for (int j = 0; j < keys; ++j) sum += (w[size_t(j)] = std::exp(w[size_t(j)] - mx));
+                double* row = O + size_t(t) * size_t(d);
+                std::fill(row, row + d, 0.0);
+                for (int j = 0; j < keys; ++j)
+                    for (int c = 0; c < d; ++c) row[c] += w[size_t(j)] * double(V(j, c));
+                for (int c = 0; c < d; ++c) row[c] /= sum;
+            }
+        }
+    return out;
+}
+
+// Tiled binary32 attention with online softmax (attention.hpp:169-252): the same
+// block traversal, causal tile classes and binary32 arithmetic order.
+inline Tensor4f flash_attention_fp(const AttentionInput& in, int block_q = 128, int block_kv = 64) {
+    if (block_q < 1 || block_kv < 1) throw std::invalid_argument("flash_attention_fp: block sizes must be >= 1");
+    b200::validate_input(in, "flash_attention_fp");
+    const int n = in.q.tokens, d = in.q.head_dim;
+    const float scale = float(1.0 / std::sqrt(double(d)));
+    const float ninf = -std::numeric_limits<float>::infinity();
+    Tensor4f out(in.q.batch, in.q.heads, n, d);
+    Matrix<float> s(block_q, block_kv), acc(block_q, d);
+    const size_t rows_per_block = static_cast<size_t>(block_q);
+    std::vector<float> m(rows_per_block), l(rows_per_block);
+    for (int b = 0; b < in.q.batch; ++b)
+        for (int h = 0; h < in.q.heads; ++h) {
+            const MatView<float> Q = in.q.slice(b, h), K = in.k.slice(b, h), V = in.v.slice(b, h);
+            float* O = out.slice_ptr(b, h);
+            for (int r0 = 0, i = 0; r0 < n; r0 += block_q, ++i) {
+                const int bq = std::min(block_q, n - r0);
+                std::fill(m.begin(), m.end(), ninf);
+                std::fill(l.begin(), l.end(), 0.0f);
+                std::fill(acc.data.begin(), acc.data.end(), 0.0f);
+                for (int c0 = 0, j = 0; c0 < n; c0 += block_kv, ++j) {
+                    const int bkv = std::min(block_kv, n - c0);
+                    TileKind kind = TileKind::Full;
+                    if (in.causal && (kind = apply_causal_tiling(i, j, block_q, block_kv, n)) == TileKind::Skip)
+                        continue;
+                    for (int r = 0; r < bq; ++r)
+                        for (int c = 0; c < bkv; ++c) {
+                            float dot = 0.0f;
+                            for (int x = 0; x < d; ++x) dot += Q(r0 + r, x) * K(c0 + c, x);
+                            s(r, c) = dot * scale;
+                            if (kind == TileKind::Diagonal && c0 + c > r0 + r) s(r, c) = ninf;
+                        }
+                    for (int r = 0; r < bq; ++r) {
+                        float mx = m[size_t(r)];
+                        for (int c = 0; c < bkv; ++c) mx = std::max(mx, s(r, c));
+                        const float alpha = std::exp(m[size_t(r)] - mx);
+                        float sum = 0.0f;
+                        for (int c = 0; c < bkv; ++c) {
+                            const float p = s(r, c) == ninf ? 0.0f : std::exp(s(r, c) - mx);
+                            s(r, c) = p;
+                            sum += p;
+                        }
+                        m[size_t(r)] = mx;
+                        l[size_t(r)] = alpha * l[size_t(r)] + sum;
+                        for (int x = 0; x < d; ++x) acc(r, x) *= alpha;
+                        for (int c = 0; c < bkv; ++c) {
+                            if (s(r, c) == 0.0f) continue;
+                            for (int x = 0; x < d; ++x) acc(r, x) += s(r, c) * V(c0 + c, x);
+                        }
+                    }
+                }
+                for (int r = 0; r < bq; ++r) {
+                    const float inv = 1.0f / l[size_t(r)];
+                    for (int x = 0; x < d; ++x) O[size_t(r0 + r) * size_t(d) + size_t(x)] = acc(r, x) * inv;
+                }
+            }
+        }
+    return out;
 }
 
 }  // namespace sageattn

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SAB_ABI_VERSION 3
+#define SAB_ABI_VERSION 4
 
 /* Status codes.  The C++ shim maps them back to the reference's exceptions:
  * SAB_ERR_SHAPE / SAB_ERR_NONFINITE / SAB_ERR_UNSUPPORTED -> std::invalid_argument,
@@ -78,6 +78,9 @@ typedef struct sab_desc {
     int32_t check_v;      /* 1: scan V for non-finite values (validate_input)      */
     int32_t qk_granularity; /* sab_qk_granularity (ABI 2)                            */
     int32_t pv_path;      /* sab_pv_path (ABI 3)                                   */
+    int32_t measure_static_scale; /* SageDiagnostics::measure_static_scale (ABI 4): INT8 P~V
+                                     path only; K2 counts static- vs per-token-scale P~ code
+                                     mismatches (attention.hpp:479-488) into the workspace */
 } sab_desc;
 
 /* Fills *d with the SAGEAttn-B defaults (kernel_config_for(B), attention.hpp:51;
@@ -102,6 +105,8 @@ typedef struct sab_ws_layout {
                            P~V path only; quantize(V, per_channel), quant.hpp:128-173) */
     uint64_t vscales;   /* float [units][head_dim] delta_V, then float [units][head_dim]
                            channel max |v| scratch (INT8 P~V path only)              */
+    uint64_t diag;      /* uint64 [2] static-scale mismatches (first KV block, later
+                           blocks); zeroed by sab_prepass (ABI 4)                     */
 } sab_ws_layout;
 
 const char* sab_status_string(int status);
@@ -150,6 +155,18 @@ int sab_read_status(const sab_desc* d, const void* ws, void* stream, int* status
 int sab_attention_fwd_host(const sab_desc* d, const void* q, const void* k, const void* v, void* o,
                            const int* devices, int n_devices);
 
+/* sab_attention_fwd_host plus the static-scale P~ diagnostics of the INT8 P~V path
+ * (SageDiagnostics, attention.hpp:58-69, 479-488): when d->measure_static_scale is set,
+ * counts[0] = P~ elements quantized (static_scale_elements), counts[1] / counts[2] =
+ * static-scale codes that differ from per-token-scale codes in the first / later KV
+ * blocks of each query block.  counts may be NULL; it is zeroed otherwise. */
+int sab_attention_fwd_host_diag(const sab_desc* d, const void* q, const void* k, const void* v, void* o,
+                                const int* devices, int n_devices, uint64_t counts[3]);
+
+/* Device path: reads the static-scale counters of the last K2 call on `ws` into
+ * counts[3] (same meaning as above); synchronous on `stream`. */
+int sab_read_static_scale_counts(const sab_desc* d, const void* ws, void* stream, uint64_t counts[3]);
+
 /* Contiguous K3 shard of `units` over `n_shards`: first unit and count of shard `s`. */
 int sab_shard_plan(int units, int n_shards, int s, int* first, int* count);
 
@@ -167,6 +184,12 @@ int sab_diagnostics(const sab_desc* d, uint64_t* s_stage_macs, uint64_t* pv_stag
 
 /* Number of visible sm_100 devices. */
 int sab_device_count(int* count);
+
+/* Ordinals of the visible sm_100 devices, ascending: writes min(count, capacity)
+ * of them to ordinals[] and the total to *count.  The drop-in passes this list
+ * to sab_attention_fwd_host so mixed-GPU hosts never place a shard on another
+ * architecture. */
+int sab_device_ordinals(int* ordinals, int capacity, int* count);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,7 @@ class Oracle:
         lib.orc_sage_v.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 9 + [_f32p, _u64p]
         lib.orc_quantize_int8_cols.argtypes = [_f32p, C.c_int, C.c_int, _i8p, _f32p]
         lib.orc_naive.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
+        lib.orc_naive_rows.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 5 + [_f64p]
         self.lib = lib
 
     # -- scalar numerics ------------------------------------------------
@@ -209,6 +210,14 @@ class Oracle:
                 raise RuntimeError(f"oracle tiles failed: {st}")
         return out
 
+    def naive_rows(self, q, k, v, causal, r0, r1):
+        """Exact binary64 attention rows [r0, r1) of ONE unit (q/k/v (N, d)); (r1 - r0, d) float64."""
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        n, d = q.shape
+        out = np.empty((r1 - r0, d), np.float64)
+        self.lib.orc_naive_rows(q, k, v, n, d, int(causal), int(r0), int(r1), out)
+        return out
+
     def naive(self, q, k, v, causal=False, threads=None):
         q, k, v = _f32(q), _f32(k), _f32(v)
         units, n, d = q.shape
@@ -245,6 +254,7 @@ class Reference:
                                          _f32p]
         lib.ref_quantize_qk_per_token.argtypes = [_f32p, _f32p] + [C.c_int] * 5 + [_i8p, _f32p, _i8p, _f32p]
         lib.ref_sage_attention_variant.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 8 + [_f32p]
+        lib.ref_static_scale_counts.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 6 + [_u64p]
         lib.ref_quantize_per_channel.argtypes = [_f32p, C.c_int, C.c_int, _i8p, _f32p]
         self.lib = lib
 
@@ -314,6 +324,17 @@ class Reference:
         if st:
             self._raise(st)
         return out
+
+    def static_scale_counts(self, q4, k4, v4, causal=False, per_token=False):
+        """SageDiagnostics static-scale counters of sage_attention(in, VB|VT) (attention.hpp:479-488):
+        (elements, first-block mismatches, later-block mismatches)."""
+        q4, k4, v4 = _f32(q4), _f32(k4), _f32(v4)
+        b, h, n, d = q4.shape
+        out = np.zeros(3, np.uint64)
+        st = self.lib.ref_static_scale_counts(q4, k4, v4, b, h, n, d, int(causal), int(per_token), out)
+        if st:
+            self._raise(st)
+        return tuple(int(x) for x in out)
 
     def quantize_per_channel(self, a):
         """quantize(a, Granularity::per_channel(), Int8): (codes (rows, cols), scales (cols,))."""

@@ -127,6 +127,24 @@ int ref_sage_attention_variant(const float* q, const float* k, const float* v, i
     }
 }
 
+// SageDiagnostics static-scale counters (attention.hpp:58-69, 479-488) of sage_attention(in,
+// VT|VB) with measure_static_scale = true: counts = {elements, first-block, later-block mismatches}.
+int ref_static_scale_counts(const float* q, const float* k, const float* v, int b, int h, int n, int d, int causal,
+                            int per_token, uint64_t* counts) {
+    try {
+        AttentionInput in{make4(q, b, h, n, d), make4(k, b, h, n, d), make4(v, b, h, n, d), causal != 0};
+        SageDiagnostics diag;
+        diag.measure_static_scale = true;
+        SageOptions opt;
+        opt.diagnostics = &diag;
+        (void)sage_attention(in, per_token ? SageVariant::VT : SageVariant::VB, opt);
+        counts[0] = diag.static_scale_elements;
+        counts[1] = diag.static_scale_first_block_mismatches;
+        counts[2] = diag.static_scale_later_block_mismatches;
+        return 0;
+    } catch (const std::invalid_argument& e) { return fail(e, 1); }
+}
+
 // quantize(a, Granularity::per_channel(), Int8) (quant.hpp:128-173): V^ of the vB/vT paths.
 int ref_quantize_per_channel(const float* a, int rows, int cols, int8_t* codes, float* scales) {
     try {

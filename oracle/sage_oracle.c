@@ -459,11 +459,15 @@ int orc_sage_b_unit(const float* q, const float* k, const float* v, int n, int d
 }
 
 /* Exact binary64 attention for one unit (attention.hpp:110-149). */
-void orc_naive_unit(const float* q, const float* k, const float* v, int n, int d, int causal, double* out)
+/* naive_attention (attention.hpp:107-149) for query rows [r0, r1) of one unit; out is
+ * (r1 - r0) x d.  Used for the exact-attention column at sizes where whole units are too
+ * slow in binary64 (bench.py parity, large-shape tests). */
+void orc_naive_rows(const float* q, const float* k, const float* v, int n, int d, int causal, int r0, int r1,
+                    double* out)
 {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);
     double* s = (double*)malloc(sizeof(double) * (size_t)n);
-    for (int t = 0; t < n; ++t) {
+    for (int t = r0; t < r1; ++t) {
         const int lim = causal ? t + 1 : n;
         double mx = -INFINITY;
         for (int j = 0; j < lim; ++j) {
@@ -474,13 +478,18 @@ void orc_naive_unit(const float* q, const float* k, const float* v, int n, int d
         }
         double den = 0.0;
         for (int j = 0; j < lim; ++j) { s[j] = exp(s[j] - mx); den += s[j]; }
-        double* orow = out + (size_t)t * d;
+        double* orow = out + (size_t)(t - r0) * d;
         for (int c = 0; c < d; ++c) orow[c] = 0.0;
         for (int j = 0; j < lim; ++j)
             for (int c = 0; c < d; ++c) orow[c] += s[j] * v[(size_t)j * d + c];
         for (int c = 0; c < d; ++c) orow[c] /= den;
     }
     free(s);
+}
+
+void orc_naive_unit(const float* q, const float* k, const float* v, int n, int d, int causal, double* out)
+{
+    orc_naive_rows(q, k, v, n, d, causal, 0, n, out);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -35,20 +35,21 @@ EXPORTS = (
     "sab_desc_init", "sab_status_string", "sab_last_error", "sab_abi_version", "sab_check_desc",
     "sab_workspace_size", "sab_workspace_layout", "sab_prepass", "sab_attention", "sab_attention_fwd",
     "sab_read_status", "sab_attention_fwd_host", "sab_shard_plan", "sab_qk_int32_tiles", "sab_diagnostics",
-    "sab_device_count",
+    "sab_device_count", "sab_device_ordinals", "sab_attention_fwd_host_diag", "sab_read_static_scale_counts",
 )
 
 
 class SabDesc(C.Structure):
     _fields_ = [(name, C.c_int32) for name in (
         "batch", "heads", "tokens", "head_dim", "causal", "in_dtype", "out_dtype", "block_q", "block_kv",
-        "smooth_k", "pv_accum", "check_v", "qk_granularity", "pv_path")]
+        "smooth_k", "pv_accum", "check_v", "qk_granularity", "pv_path", "measure_static_scale")]
 
 
 class SabWsLayout(C.Structure):
     _fields_ = [(name, C.c_uint64) for name in (
         "qcodes", "kcodes", "qscales", "kscales", "mean_k", "partials", "v16", "status", "total")] + [
-        ("n_partials", C.c_int32), ("tree_depth", C.c_int32), ("vcodes", C.c_uint64), ("vscales", C.c_uint64)]
+        ("n_partials", C.c_int32), ("tree_depth", C.c_int32), ("vcodes", C.c_uint64), ("vscales", C.c_uint64),
+        ("diag", C.c_uint64)]
 
 
 class SabError(RuntimeError):
@@ -90,6 +91,9 @@ def load():
     lib.sab_qk_int32_tiles.argtypes = [P(SabDesc), vp, C.c_int, C.c_int, vp, vp]
     lib.sab_diagnostics.argtypes = [P(SabDesc), P(C.c_uint64), P(C.c_uint64)]
     lib.sab_device_count.argtypes = [P(C.c_int)]
+    lib.sab_device_ordinals.argtypes = [P(C.c_int), C.c_int, P(C.c_int)]
+    lib.sab_attention_fwd_host_diag.argtypes = [P(SabDesc), vp, vp, vp, vp, P(C.c_int), C.c_int, P(C.c_uint64)]
+    lib.sab_read_static_scale_counts.argtypes = [P(SabDesc), vp, vp, P(C.c_uint64)]
     for name in EXPORTS:
         if name not in ("sab_desc_init", "sab_status_string", "sab_last_error"):
             getattr(lib, name).restype = C.c_int
@@ -128,6 +132,15 @@ def shard_plan(units: int, n_shards: int, s: int):
     first, count = C.c_int(), C.c_int()
     check(load().sab_shard_plan(units, n_shards, s, C.byref(first), C.byref(count)))
     return first.value, count.value
+
+
+def device_ordinals():
+    """Ordinals of the visible sm_100 devices (sab_device_ordinals)."""
+    n = C.c_int()
+    check(load().sab_device_ordinals(None, 0, C.byref(n)))
+    arr = (C.c_int * max(1, n.value))()
+    check(load().sab_device_ordinals(arr, n.value, C.byref(n)))
+    return list(arr[:n.value])
 
 
 def diagnostics(d: SabDesc):

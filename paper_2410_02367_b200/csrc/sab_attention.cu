@@ -275,15 +275,41 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
     return alpha;
 }
 
+// SageDiagnostics::measure_static_scale (attention.hpp:479-488): the per-token-scale codes
+// of this tile row (quantize(P~, per_token, Int8), quant.hpp:128-173: delta = max/127,
+// inv = 1/delta, clamp(rint(p * inv))) against the static-scale codes rint(p * 127)
+// (quantize_p_static, quant.hpp:258-279).  p holds this thread's 32 values of the row
+// (masked entries 0); the row's two threads meet by a shuffle.  Rows past the last
+// token are not part of the reference's tile and are skipped.
+__device__ __forceinline__ void count_static_scale_mismatches(const float (&p)[32], bool row_valid, bool first,
+                                                              unsigned long long* diag) {
+    float pm = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) pm = fmaxf(pm, p[c]);
+    pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, 16));
+    const float delta = pm == 0.0f ? 1.0f : __fdiv_rn(pm, 127.0f);
+    const float inv = pm == 0.0f ? 0.0f : __fdiv_rn(1.0f, delta);
+    int mism = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        const float cs = fminf(rintf(__fmul_rn(p[c], 127.0f)), 127.0f);
+        const float ct = fminf(fmaxf(rintf(__fmul_rn(p[c], inv)), -127.0f), 127.0f);
+        mism += cs != ct;
+    }
+    mism = __reduce_add_sync(0xffffffffu, row_valid ? mism : 0);
+    if ((threadIdx.x & 31) == 0 && mism) atomicAdd(diag + (first ? 0 : 1), static_cast<unsigned long long>(mism));
+}
+
 // SAGEAttn-vB variant of softmax_half (INT8 P~V, attention.hpp:476-505): the running max
 // is exact (no lazy threshold) so every p lies in [0, 1], and P~ is stored as the static-scale
 // codes rne(p * 127) (quantize_p_static, quant.hpp:258-279), four per TMEM column (thread t's
 // 8 words go to columns [8*half, 8*half + 8)), the A operand of the kind::i8 PV MMA.  All
 // exponentials are MUFU ex2 of float(acc) * cg - m (one rounding), so the codes are the
 // reference's up to an ulp of the exponent.  Returns the O rescale factor 2^(m_old - m).
-template <bool MASK, bool CAUSAL>
+template <bool MASK, bool CAUSAL, bool DIAG>
 __device__ __forceinline__ float softmax_half_i8(const uint32_t (&r)[32], uint32_t ts, int half, float cg, int kb,
-                                                 int qi, int n, float& m, float& l, bool& rescale) {
+                                                 int qi, int n, float& m, float& l, bool& rescale,
+                                                 unsigned long long* diag, bool first) {
     const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
     int imax = group_max<MASK>(r, lim);
     imax = max(imax, __shfl_xor_sync(0xffffffffu, imax, 16));
@@ -297,6 +323,7 @@ __device__ __forceinline__ float softmax_half_i8(const uint32_t (&r)[32], uint32
     const int lim2 = MASK ? opaque(lim) : lim;
     f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
     uint32_t pk[8];
+    float pd[DIAG ? 32 : 1];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         uint32_t b[4];
@@ -310,6 +337,10 @@ __device__ __forceinline__ float softmax_half_i8(const uint32_t (&r)[32], uint32
                 pp.x = (c >= lim2) ? 0.0f : pp.x;
                 pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
             }
+            if (DIAG) {
+                pd[c] = pp.x;
+                pd[c + 1] = pp.y;
+            }
             acc[(2 * i + e / 2) & 3] = fadd2(acc[(2 * i + e / 2) & 3], pp);
             // rne(p * 127): the product rounded to binary32 (quant.hpp:96), then 2^23 + 2^22
             // added so the code sits in the low mantissa byte.
@@ -320,6 +351,7 @@ __device__ __forceinline__ float softmax_half_i8(const uint32_t (&r)[32], uint32
         pk[i] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
     }
     tmem_st16x2_8(ts, pk);
+    if (DIAG) count_static_scale_mismatches(reinterpret_cast<const float(&)[32]>(pd), qi < n, first, diag);
     const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
     l = fmaf(l, alpha, sum.x + sum.y);
     return alpha;
@@ -442,10 +474,10 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
 
 // SAGEAttn-vT: per-token scales (softmax_half_pt's exact pass) with the vB P~ store:
 // scores w*acc per element, exact row max, MUFU exponentials, static-scale INT8 codes.
-template <bool MASK, bool CAUSAL>
+template <bool MASK, bool CAUSAL, bool DIAG>
 __device__ __forceinline__ float softmax_half_pt_i8(uint32_t (&r)[32], uint32_t ts, int half, float dq,
                                                     const float* dkp, int kb, int qi, int n, float& m, float& l,
-                                                    bool& rescale) {
+                                                    bool& rescale, unsigned long long* diag, bool first) {
     const int lim = (CAUSAL ? min(n, qi + 1) : n) - kb - 32 * half;
     const int lim2 = MASK ? opaque(lim) : lim;
     float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -477,6 +509,7 @@ __device__ __forceinline__ float softmax_half_pt_i8(uint32_t (&r)[32], uint32_t 
     const float mref = (m == -INFINITY) ? 0.0f : m;
     f2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
     uint32_t pk[8];
+    float pd[DIAG ? 32 : 1];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         uint32_t b[4];
@@ -489,6 +522,10 @@ __device__ __forceinline__ float softmax_half_pt_i8(uint32_t (&r)[32], uint32_t 
                 pp.x = (c >= lim2) ? 0.0f : pp.x;
                 pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
             }
+            if (DIAG) {
+                pd[c] = pp.x;
+                pd[c + 1] = pp.y;
+            }
             acc[(2 * i + e / 2) & 3] = fadd2(acc[(2 * i + e / 2) & 3], pp);
             const f2 q = fadd2(ffma2(pp, f2{127.0f, 127.0f}, f2{0.0f, 0.0f}), f2{kMagicF, kMagicF});
             b[e] = __float_as_uint(q.x);
@@ -497,6 +534,7 @@ __device__ __forceinline__ float softmax_half_pt_i8(uint32_t (&r)[32], uint32_t 
         pk[i] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
     }
     tmem_st16x2_8(ts, pk);
+    if (DIAG) count_static_scale_mismatches(reinterpret_cast<const float(&)[32]>(pd), qi < n, first, diag);
     const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
     l = fmaf(l, alpha, sum.x + sum.y);
     return alpha;
@@ -747,15 +785,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float alpha;
                 if (VI8 && PT) {
                     const float* dkp = ksc + kb + 32 * half;
-                    if (need_mask)
-                        alpha = softmax_half_pt_i8<true, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale);
+                    if (p.diag)  // static-scale diagnostics (rare, slow path)
+                        alpha = need_mask ? softmax_half_pt_i8<true, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, qi, n, m,
+                                                                                   l, rescale, p.diag, j == 0)
+                                          : softmax_half_pt_i8<false, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, qi, n,
+                                                                                    m, l, rescale, p.diag, j == 0);
+                    else if (need_mask)
+                        alpha = softmax_half_pt_i8<true, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale,
+                                                                        nullptr, false);
                     else
-                        alpha = softmax_half_pt_i8<false, CAUSAL>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale);
+                        alpha = softmax_half_pt_i8<false, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, qi, n, m, l,
+                                                                         rescale, nullptr, false);
                 } else if (VI8) {
-                    if (need_mask)
-                        alpha = softmax_half_i8<true, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale);
+                    if (p.diag)
+                        alpha = need_mask ? softmax_half_i8<true, CAUSAL, true>(r, t_s, half, cg, kb, qi, n, m, l,
+                                                                                rescale, p.diag, j == 0)
+                                          : softmax_half_i8<false, CAUSAL, true>(r, t_s, half, cg, kb, qi, n, m, l,
+                                                                                 rescale, p.diag, j == 0);
+                    else if (need_mask)
+                        alpha = softmax_half_i8<true, CAUSAL, false>(r, t_s, half, cg, kb, qi, n, m, l, rescale,
+                                                                     nullptr, false);
                     else
-                        alpha = softmax_half_i8<false, CAUSAL>(r, t_s, half, cg, kb, qi, n, m, l, rescale);
+                        alpha = softmax_half_i8<false, CAUSAL, false>(r, t_s, half, cg, kb, qi, n, m, l, rescale,
+                                                                      nullptr, false);
                 } else if (PT) {
                     const float* dkp = ksc + kb + 32 * half;
                     if (need_mask)

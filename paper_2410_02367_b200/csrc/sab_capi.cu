@@ -64,6 +64,7 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     L->status = take(sizeof(int32_t) * (1 + units));  // status word + per-unit K1 counters
     L->vcodes = take(pv8 ? units * hd * npad : 0);
     L->vscales = take(pv8 ? 2 * units * hd * sizeof(float) : 0);
+    L->diag = take(2 * sizeof(unsigned long long));
     L->total = off;
     L->n_partials = n_partials;
     L->tree_depth = depth;
@@ -134,6 +135,7 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
     a.causal = d->causal != 0;
     a.out_f32 = d->out_dtype == SAB_F32;
     a.per_token = d->qk_granularity == SAB_QK_PER_TOKEN;
+    a.diag = (pv8 && d->measure_static_scale) ? at<unsigned long long>(w, L.diag) : nullptr;
     return a;
 }
 
@@ -149,6 +151,7 @@ int enqueue_prepass(const sab_desc* d, const sab_ws_layout& L, const void* q, co
         return set_error(SAB_ERR_UNSUPPORTED, "sab_prepass: batch*heads above 65535 per device call");
     if (reset) {
         cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t) * (1 + size_t(units_of(d))), s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(at<uint8_t>(ws, L.diag), 0, 2 * sizeof(unsigned long long), s);
         if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: status reset");
     }
     cudaError_t e = launch_prepass(prepass_params(d, L, q, k, v, ws), s);
@@ -160,6 +163,14 @@ int enqueue_attention(const sab_desc* d, const sab_ws_layout& L, void* ws, const
     cudaError_t e = launch_attention(attn_params(d, L, ws, v, o), s);
     if (e != cudaSuccess) return cuda_fail(e, "sab_attention: launch");
     return SAB_OK;
+}
+
+// Elements quantize_p_static sees (attention.hpp:485): bq * bkv per non-skipped tile,
+// i.e. the S-stage MACs divided by head_dim.
+uint64_t static_scale_elements(const sab_desc* d) {
+    uint64_t s = 0, p = 0;
+    if (sab_diagnostics(d, &s, &p) != SAB_OK) return 0;
+    return s / uint64_t(d->head_dim);
 }
 
 int map_status_word(int word) {
@@ -232,6 +243,12 @@ int sab_check_desc(const sab_desc* d) {
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: only the FP32-accumulator P~V arm is implemented");
     if (units_of(d) > (int64_t(1) << 24))
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: batch*heads too large");
+    // The INT8 P~V path accumulates P~^ V^ in one INT32 TMEM accumulator per row over all
+    // keys: each key adds at most 127 * 127, so more than 2^31 / 16129 keys could wrap it.
+    if (d->pv_path == SAB_PV_PATH_INT8 && d->tokens > kMaxTokensInt8Pv)
+        return set_error(SAB_ERR_UNSUPPORTED,
+                         "sage_attention: the INT8 P~V path (vB/vT) supports at most 133144 tokens "
+                         "(INT32 P~V accumulator)");
     return SAB_OK;
 }
 
@@ -328,21 +345,27 @@ int sab_diagnostics(const sab_desc* d, uint64_t* s_stage_macs, uint64_t* pv_stag
     return SAB_OK;
 }
 
-int sab_device_count(int* count) {
-    if (!count) return set_error(SAB_ERR_ARGUMENT, "count is NULL");
+int sab_device_ordinals(int* ordinals, int capacity, int* count) {
+    if (!count || (capacity > 0 && !ordinals)) return set_error(SAB_ERR_ARGUMENT, "sab_device_ordinals: NULL argument");
     int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess) {
-        *count = 0;
-        return SAB_OK;
-    }
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
     int c = 0;
     for (int i = 0; i < n; ++i) {
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, i) == cudaSuccess && prop.major == 10 && prop.minor == 0) ++c;
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, i) == cudaSuccess &&
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, i) == cudaSuccess && major == 10 &&
+            minor == 0) {
+            if (c < capacity) ordinals[c] = i;
+            ++c;
+        }
     }
     *count = c;
     return SAB_OK;
+}
+
+int sab_device_count(int* count) {
+    if (!count) return set_error(SAB_ERR_ARGUMENT, "count is NULL");
+    return sab_device_ordinals(nullptr, 0, count);
 }
 
 int sab_qk_int32_tiles(const sab_desc* d, const void* ws, int unit, int q_tile, int32_t* s_out, void* stream) {
@@ -366,16 +389,20 @@ int sab_qk_int32_tiles(const sab_desc* d, const void* ws, int unit, int q_tile, 
 namespace {
 
 // Per-device execution context of the host-buffer path: three streams
-// (H2D / compute / D2H), per-chunk events and grow-only device buffers.
-// Contexts are pooled so repeated calls do not pay cudaMalloc/stream
+// (H2D / compute / D2H), per-chunk events, grow-only device buffers and, for
+// pageable caller buffers, two pinned staging slots per direction.  Contexts
+// are pooled so repeated calls do not pay cudaMalloc / cudaHostAlloc / stream
 // creation; a context is owned by one call at a time, so concurrent callers
 // never share buffers (the reference entry is re-entrant, attention.hpp:9-12).
 struct DevCtx {
     int device = -1;
     cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
-    std::vector<cudaEvent_t> ev_in, ev_cmp;
+    std::vector<cudaEvent_t> ev_in, ev_cmp, ev_out;
     uint8_t* buf = nullptr;
     size_t buf_bytes = 0;
+    uint8_t* pin_in[2] = {nullptr, nullptr};   // staging of Q, K, V chunks
+    uint8_t* pin_out[2] = {nullptr, nullptr};  // staging of O chunks
+    size_t pin_in_bytes = 0, pin_out_bytes = 0;
 };
 
 std::mutex g_pool_mu;
@@ -390,11 +417,13 @@ cudaError_t ctx_reserve(DevCtx* c, size_t bytes, int n_events) {
             return e;
     }
     while (int(c->ev_in.size()) < n_events) {
-        cudaEvent_t a, b;
+        cudaEvent_t a, b, o;
         if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&o, cudaEventDisableTiming)) != cudaSuccess) return e;
         c->ev_in.push_back(a);
         c->ev_cmp.push_back(b);
+        c->ev_out.push_back(o);
     }
     if (c->buf_bytes < bytes) {
         if (c->buf) cudaFree(c->buf);
@@ -402,6 +431,33 @@ cudaError_t ctx_reserve(DevCtx* c, size_t bytes, int n_events) {
         c->buf_bytes = 0;
         if ((e = cudaMalloc(&c->buf, bytes)) != cudaSuccess) return e;
         c->buf_bytes = bytes;
+    }
+    return e;
+}
+
+cudaError_t ctx_reserve_pinned(DevCtx* c, size_t in_bytes, size_t out_bytes) {
+    cudaError_t e = cudaSuccess;
+    if (c->pin_in_bytes < in_bytes) {
+        for (auto& p : c->pin_in) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+        }
+        c->pin_in_bytes = 0;
+        for (auto& p : c->pin_in)
+            if ((e = cudaHostAlloc(reinterpret_cast<void**>(&p), in_bytes, cudaHostAllocPortable)) != cudaSuccess)
+                return e;
+        c->pin_in_bytes = in_bytes;
+    }
+    if (c->pin_out_bytes < out_bytes) {
+        for (auto& p : c->pin_out) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+        }
+        c->pin_out_bytes = 0;
+        for (auto& p : c->pin_out)
+            if ((e = cudaHostAlloc(reinterpret_cast<void**>(&p), out_bytes, cudaHostAllocPortable)) != cudaSuccess)
+                return e;
+        c->pin_out_bytes = out_bytes;
     }
     return e;
 }
@@ -425,14 +481,48 @@ void ctx_release(DevCtx* c) {
     g_pool.push_back(c);
 }
 
+// True when `p` is ordinary pageable host memory (not cudaHostAlloc'ed or
+// registered): copies from it would serialise behind the driver's own bounce
+// buffer, so the host path stages it through pinned slots instead.
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// memcpy split over `threads` host threads (host memory bandwidth needs several
+// cores; one core copies at roughly a third of PCIe Gen5 speed).
+void par_copy(void* dst, const void* src, size_t bytes, int threads) {
+    constexpr size_t kMinPiece = size_t(4) << 20;
+    threads = int(std::max<size_t>(1, std::min<size_t>(size_t(threads), bytes / kMinPiece)));
+    if (threads <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t piece = (bytes + threads - 1) / threads;
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) {
+        const size_t a = size_t(t) * piece, b = std::min(bytes, a + piece);
+        if (a < b)
+            pool.emplace_back([=] { std::memcpy(static_cast<uint8_t*>(dst) + a, static_cast<const uint8_t*>(src) + a, b - a); });
+    }
+    std::memcpy(dst, src, std::min(bytes, piece));
+    for (auto& t : pool) t.join();
+}
+
 struct ShardJob {
     const sab_desc* desc;
     const uint8_t *q, *k, *v;
     uint8_t* o;
     int device;
     int first, count;
+    int copy_threads;  // host threads per staging copy
     int status;
     std::string error;
+    unsigned long long mismatches[2] = {0, 0};  // static-scale P~ diagnostics of this shard
 };
 
 int run_shard_on(ShardJob* job, DevCtx* ctx) {
@@ -460,46 +550,93 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     const size_t out_bytes = align_up(size_t(job->count) * unit_elems * out_e, 256);
     cudaError_t e = ctx_reserve(ctx, 3 * in_bytes + out_bytes + L.total, n_chunks);
     if (e != cudaSuccess) return cuda_fail(e, "sab_attention_fwd_host: device buffers");
-    uint8_t* dq = ctx->buf;
-    uint8_t* dk = dq + in_bytes;
-    uint8_t* dv = dk + in_bytes;
-    uint8_t* dout = dv + in_bytes;
+    // Pageable caller buffers go through two pinned slots per direction: the host
+    // thread copies chunk c into slot c % 2 while the GPU reads chunk c - 1 from the
+    // other slot (and the same, reversed, for O).
+    const uint8_t* src_in[3] = {job->q, job->k, job->v};
+    bool stage_in[3], stage_out = is_pageable(job->o);
+    bool any_in = false;
+    for (int t = 0; t < 3; ++t) any_in |= (stage_in[t] = is_pageable(src_in[t]));
+    const size_t chunk_in = size_t(chunk) * unit_elems * in_e, chunk_out = size_t(chunk) * unit_elems * out_e;
+    if (any_in || stage_out) {
+        e = ctx_reserve_pinned(ctx, any_in ? 3 * chunk_in : 0, stage_out ? chunk_out : 0);
+        if (e != cudaSuccess) return cuda_fail(e, "sab_attention_fwd_host: pinned staging buffers");
+    }
+    uint8_t* dev_in[3] = {ctx->buf, ctx->buf + in_bytes, ctx->buf + 2 * in_bytes};
+    uint8_t* dout = ctx->buf + 3 * in_bytes;
     uint8_t* ws = dout + out_bytes;
 
-    if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t) * (1 + size_t(chunk)), ctx->s_cmp)) != cudaSuccess)
+    if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t) * (1 + size_t(chunk)), ctx->s_cmp)) != cudaSuccess ||
+        (e = cudaMemsetAsync(ws + L.diag, 0, 2 * sizeof(unsigned long long), ctx->s_cmp)) != cudaSuccess)
         return cuda_fail(e, "sab_attention_fwd_host: memset");
+    // Copies the finished O of chunk c out of its pinned slot into the caller's buffer.
+    auto drain_out = [&](int c) -> cudaError_t {
+        const int u0 = c * chunk, cu = std::min(chunk, job->count - u0);
+        cudaError_t x = cudaEventSynchronize(ctx->ev_out[c]);
+        if (x == cudaSuccess)
+            par_copy(job->o + size_t(u0) * unit_elems * out_e, ctx->pin_out[c % 2], size_t(cu) * unit_elems * out_e,
+                     job->copy_threads);
+        return x;
+    };
     int st = SAB_OK;
     for (int c = 0; c < n_chunks && st == SAB_OK; ++c) {
         const int u0 = c * chunk, cu = std::min(chunk, job->count - u0);
         const size_t ioff = size_t(u0) * unit_elems * in_e, ibytes = size_t(cu) * unit_elems * in_e;
         const size_t ooff = size_t(u0) * unit_elems * out_e, obytes = size_t(cu) * unit_elems * out_e;
-        if ((e = cudaMemcpyAsync(dq + ioff, job->q + ioff, ibytes, cudaMemcpyHostToDevice, ctx->s_in)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(dk + ioff, job->k + ioff, ibytes, cudaMemcpyHostToDevice, ctx->s_in)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(dv + ioff, job->v + ioff, ibytes, cudaMemcpyHostToDevice, ctx->s_in)) != cudaSuccess ||
-            (e = cudaEventRecord(ctx->ev_in[c], ctx->s_in)) != cudaSuccess ||
+        const int slot = c % 2;
+        // The slot was last read by the H2D of chunk c - 2.
+        if (any_in && c >= 2 && (e = cudaEventSynchronize(ctx->ev_in[c - 2])) != cudaSuccess) {
+            st = cuda_fail(e, "sab_attention_fwd_host: staging");
+            break;
+        }
+        for (int t = 0; t < 3 && e == cudaSuccess; ++t) {
+            const uint8_t* from = src_in[t] + ioff;
+            if (stage_in[t]) {
+                uint8_t* pinned = ctx->pin_in[slot] + size_t(t) * chunk_in;
+                par_copy(pinned, from, ibytes, job->copy_threads);
+                from = pinned;
+            }
+            e = cudaMemcpyAsync(dev_in[t] + ioff, from, ibytes, cudaMemcpyHostToDevice, ctx->s_in);
+        }
+        if (e != cudaSuccess || (e = cudaEventRecord(ctx->ev_in[c], ctx->s_in)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(ctx->s_cmp, ctx->ev_in[c], 0)) != cudaSuccess) {
             st = cuda_fail(e, "sab_attention_fwd_host: H2D");
             break;
         }
+        // A short last chunk keeps the full-chunk layout L (every region is sized for
+        // `chunk` units, so `cu` units fit): only the unit count changes.  A layout
+        // recomputed for `cu` units would move the regions after the status word
+        // (V^ / delta_V of the INT8 P~V path) on top of it.
         sab_desc xd = cd;
         xd.heads = cu;
-        sab_ws_layout XL;
-        layout_of(&xd, &XL);
-        XL.status = L.status;  // one status word for the whole shard
-        if ((st = enqueue_prepass(&xd, XL, dq + ioff, dk + ioff, dv + ioff, ws, ctx->s_cmp, false)) != SAB_OK) break;
-        if ((st = enqueue_attention(&xd, XL, ws, dv + ioff, dout + ooff, ctx->s_cmp)) != SAB_OK) break;
+        if ((st = enqueue_prepass(&xd, L, dev_in[0] + ioff, dev_in[1] + ioff, dev_in[2] + ioff, ws, ctx->s_cmp,
+                                  false)) != SAB_OK)
+            break;
+        if ((st = enqueue_attention(&xd, L, ws, dev_in[2] + ioff, dout + ooff, ctx->s_cmp)) != SAB_OK) break;
+        // The O slot of chunk c was last filled by chunk c - 2, drained below at step c - 1.
         if ((e = cudaEventRecord(ctx->ev_cmp[c], ctx->s_cmp)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(ctx->s_out, ctx->ev_cmp[c], 0)) != cudaSuccess ||
-            (e = cudaMemcpyAsync(job->o + ooff, dout + ooff, obytes, cudaMemcpyDeviceToHost, ctx->s_out)) !=
-                cudaSuccess) {
+            (e = cudaMemcpyAsync(stage_out ? ctx->pin_out[slot] : job->o + ooff, dout + ooff, obytes,
+                                 cudaMemcpyDeviceToHost, ctx->s_out)) != cudaSuccess ||
+            (e = cudaEventRecord(ctx->ev_out[c], ctx->s_out)) != cudaSuccess) {
             st = cuda_fail(e, "sab_attention_fwd_host: D2H");
             break;
         }
+        if (stage_out && c >= 1 && (e = drain_out(c - 1)) != cudaSuccess) {
+            st = cuda_fail(e, "sab_attention_fwd_host: D2H staging");
+            break;
+        }
     }
+    if (st == SAB_OK && stage_out && (e = drain_out(n_chunks - 1)) != cudaSuccess)
+        st = cuda_fail(e, "sab_attention_fwd_host: D2H staging");
     int word = 0;
     if (st == SAB_OK &&
         (e = cudaMemcpyAsync(&word, ws + L.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->s_cmp)) != cudaSuccess)
         st = cuda_fail(e, "sab_attention_fwd_host: status");
+    if (st == SAB_OK && D->measure_static_scale &&
+        (e = cudaMemcpyAsync(job->mismatches, ws + L.diag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             ctx->s_cmp)) != cudaSuccess)
+        st = cuda_fail(e, "sab_attention_fwd_host: diagnostics");
     // Always drain all three streams before the context is reused.
     cudaError_t e1 = cudaStreamSynchronize(ctx->s_in), e2 = cudaStreamSynchronize(ctx->s_cmp),
                 e3 = cudaStreamSynchronize(ctx->s_out);
@@ -511,7 +648,20 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     return st;
 }
 
+// Restores the calling thread's current device on scope exit: the single-device
+// call runs its shard on the caller's thread and must not leave it switched.
+struct DeviceGuard {
+    int saved = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&saved) != cudaSuccess) saved = -1;
+    }
+    ~DeviceGuard() {
+        if (saved >= 0) cudaSetDevice(saved);
+    }
+};
+
 void run_shard(ShardJob* job) {
+    DeviceGuard guard;
     cudaError_t e = cudaSetDevice(job->device);
     int st;
     if (e != cudaSuccess) {
@@ -529,6 +679,12 @@ void run_shard(ShardJob* job) {
 
 int sab_attention_fwd_host(const sab_desc* d, const void* q, const void* k, const void* v, void* o,
                            const int* devices, int n_devices) {
+    return sab_attention_fwd_host_diag(d, q, k, v, o, devices, n_devices, nullptr);
+}
+
+int sab_attention_fwd_host_diag(const sab_desc* d, const void* q, const void* k, const void* v, void* o,
+                                const int* devices, int n_devices, uint64_t counts[3]) {
+    if (counts) counts[0] = counts[1] = counts[2] = 0;
     int st = sab_check_desc(d);
     if (st) return st;
     if (!q || !k || !v || !o) return set_error(SAB_ERR_ARGUMENT, "sab_attention_fwd_host: NULL buffer");
@@ -555,6 +711,7 @@ int sab_attention_fwd_host(const sab_desc* d, const void* q, const void* k, cons
         j.k = static_cast<const uint8_t*>(k) + j.first * in_unit;
         j.v = static_cast<const uint8_t*>(v) + j.first * in_unit;
         j.o = static_cast<uint8_t*>(o) + j.first * out_unit;
+        j.copy_threads = std::max(1, std::min(8, int(std::thread::hardware_concurrency()) / n_devices));
         j.status = SAB_OK;
     }
     if (n_devices == 1) {
@@ -576,6 +733,30 @@ int sab_attention_fwd_host(const sab_desc* d, const void* q, const void* k, cons
         }
     }
     if (worst != SAB_OK) return set_error(worst, msg);
+    if (counts && d->measure_static_scale && d->pv_path == SAB_PV_PATH_INT8) {
+        counts[0] = static_scale_elements(d);
+        for (auto& j : jobs) {
+            counts[1] += j.mismatches[0];
+            counts[2] += j.mismatches[1];
+        }
+    }
+    return SAB_OK;
+}
+
+int sab_read_static_scale_counts(const sab_desc* d, const void* ws, void* stream, uint64_t counts[3]) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    if (!ws || !counts) return set_error(SAB_ERR_ARGUMENT, "sab_read_static_scale_counts: NULL argument");
+    unsigned long long m[2] = {0, 0};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(m, at<uint8_t>(const_cast<void*>(ws), L.diag), sizeof(m), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_read_static_scale_counts");
+    const bool on = d->measure_static_scale && d->pv_path == SAB_PV_PATH_INT8;
+    counts[0] = on ? static_scale_elements(d) : 0;
+    counts[1] = on ? m[0] : 0;
+    counts[2] = on ? m[1] : 0;
     return SAB_OK;
 }
 

@@ -14,6 +14,8 @@ namespace sab {
 constexpr int kBlockQ = 128;    // query tile = Q quantization group (attention.hpp:51, 344)
 constexpr int kBlockKV = 64;    // K quantization group (attention.hpp:51, 345)
 constexpr int kTileN = 64;      // keys per K2 KV tile (one K group)
+// vB/vT: INT32 P~^V^ accumulator bound, floor((2^31 - 1) / (127 * 127)) keys.
+constexpr int kMaxTokensInt8Pv = 133144;
 
 // Device status word bits (mapped to sab_status by sab_read_status).
 constexpr int kStatusNonFinite = 1;
@@ -70,6 +72,7 @@ struct AttnParams {
     int units, n, d, causal, out_f32, per_token;
     int dump_unit, dump_qtile;
     int group_units;  // K2 raster: units per L2-resident group (set by launch_attention)
+    unsigned long long* diag;  // vB/vT static-scale P~ mismatches [first block, later blocks], or NULL
 };
 
 cudaError_t launch_attention(const AttnParams& p, cudaStream_t s);

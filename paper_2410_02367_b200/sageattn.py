@@ -10,8 +10,9 @@ Names, argument meaning and error behaviour follow
 * ``sage_attention(inp, config_or_variant, options)`` (318-319, 547-550)
   runs on B200 through ``sab_attention_fwd_host``: ValueError stands for
   std::invalid_argument and OverflowError for std::overflow_error, with the
-  reference's messages.  Options outside the SAGEAttn-B hot path (T/vT/vB,
-  FP8 dtypes, other block sizes) raise ValueError -- there is no CPU fallback.
+  reference's messages.  All four variants (B, T, vB, vT) run; options outside
+  them (FP8 dtypes, PerTensor scales, other block sizes, head_dim not 64/128)
+  raise ValueError -- there is no CPU fallback.
 
 ``sage_attention_cuda`` is the device-resident path for torch CUDA tensors
 (fp16 in, fp16/fp32 out) used by bench.py; ``prepass_cuda`` and
@@ -164,14 +165,22 @@ def sage_attention(inp: AttentionInput, config: Union[KernelConfig, SageVariant]
                          smooth_k=options.smooth_k, check_v=True,
                          per_token=config.qk_granularity == QkGranularity.PerToken,
                          pv_int8=config.pv_path == PvPath.Int8)
+        diag = options.diagnostics
+        desc.measure_static_scale = int(diag is not None and diag.measure_static_scale
+                                        and config.pv_path == PvPath.Int8)
         devs = list(devices) if devices else [0]
         arr = (C.c_int * len(devs))(*devs)
-        _lib.check(_lib.load().sab_attention_fwd_host(C.byref(desc), q.ctypes.data, k.ctypes.data, v.ctypes.data,
-                                                      out.ctypes.data, arr, len(devs)))
-        if options.diagnostics is not None:
+        counts = (C.c_uint64 * 3)()
+        _lib.check(_lib.load().sab_attention_fwd_host_diag(C.byref(desc), q.ctypes.data, k.ctypes.data,
+                                                           v.ctypes.data, out.ctypes.data, arr, len(devs), counts))
+        if diag is not None:
             s, p = _lib.diagnostics(desc)
-            options.diagnostics.s_stage_macs += s
-            options.diagnostics.pv_stage_macs += p
+            diag.s_stage_macs += s
+            diag.pv_stage_macs += p
+            if desc.measure_static_scale:  # attention.hpp:479-488, counted by K2 on the GPU
+                diag.static_scale_elements += counts[0]
+                diag.static_scale_first_block_mismatches += counts[1]
+                diag.static_scale_later_block_mismatches += counts[2]
     except _lib.SabError as e:
         _raise_for(e)
     return out

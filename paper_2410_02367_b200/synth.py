@@ -57,3 +57,39 @@ def qkv(units: int, n: int, d: int, unit0: int = 0, dtype=np.float16, dist: str 
     """Q (seed 1), K (seed 2, `dist`), V (seed 3)."""
     shape = (units, n, d)
     return (tensor(1, shape, unit0, dtype), tensor(2, shape, unit0, dtype, dist=dist), tensor(3, shape, unit0, dtype))
+
+
+def tensor_torch(seed: int, shape, unit0: int = 0, device="cuda", dtype=None, chunk_units: int = 8):
+    """Same counter-based N(0,1) values as ``tensor(..., dist="normal")``, generated with torch on
+    `device` (the bench's full-size inputs; numpy would take minutes at C4/C5 sizes).
+
+    splitmix64 runs in int64 with wrap-around multiplies and masked (logical) right shifts;
+    Box-Muller runs in float64, so values equal the numpy ones up to the last ulp of the
+    binary64 log/cos before the fp16 rounding (a handful of fp16 ties can differ)."""
+    import torch
+
+    dtype = dtype or torch.float16
+    units, n, d = shape
+    per = n * d
+    out = torch.empty((units, n, d), dtype=dtype, device=device)
+
+    def u64(x: int) -> int:  # the int64 with the same 64 bits
+        return x - (1 << 64) if x >= (1 << 63) else x
+
+    def lsr(x, s):
+        return (x >> s) & ((1 << (64 - s)) - 1)
+
+    gold, m1, m2 = u64(0x9E3779B97F4A7C15), u64(0xBF58476D1CE4E5B9), u64(0x94D049BB133111EB)
+    key = u64((seed * 0xD1B54A32D192ED03) % (1 << 64))
+    for u0 in range(0, units, chunk_units):
+        uc = min(chunk_units, units - u0)
+        idx = torch.arange((unit0 + u0) * per, (unit0 + u0 + uc) * per, dtype=torch.int64, device=device)
+        z = (idx ^ key) + gold
+        z = (z ^ lsr(z, 30)) * m1
+        z = (z ^ lsr(z, 27)) * m2
+        h = z ^ lsr(z, 31)
+        u1 = (lsr(h, 40).to(torch.float64) + 0.5) * (1.0 / (1 << 24))
+        u2 = ((h & 0xFFFFFF).to(torch.float64) + 0.5) * (1.0 / (1 << 24))
+        val = torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * torch.pi * u2)
+        out[u0:u0 + uc] = val.reshape(uc, n, d).to(torch.float16).to(dtype)
+    return out

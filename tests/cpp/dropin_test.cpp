@@ -6,6 +6,8 @@
 // error contract.  Prints "MACS <s> <pv>" and "ERRORS OK".
 #include <sageattn/attention.hpp>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -60,6 +62,40 @@ int main(int argc, char** argv) {
     std::ofstream(std::string(argv[9]) + ".vt", std::ios::binary)
         .write(reinterpret_cast<const char*>(out_vt.data.data()), std::streamsize(out_vt.size() * sizeof(float)));
     std::printf("MACS %llu %llu\n", (unsigned long long)diag.s_stage_macs, (unsigned long long)diag.pv_stage_macs);
+    // Static-scale P~ diagnostics of the INT8 P~V path (attention.hpp:479-488).
+    sageattn::SageDiagnostics sdiag;
+    sdiag.measure_static_scale = true;
+    sageattn::SageOptions sopts;
+    sopts.diagnostics = &sdiag;
+    (void)sageattn::sage_attention(in, sageattn::SageVariant::VB, sopts);
+    std::printf("STATIC %llu %llu %llu\n", (unsigned long long)sdiag.static_scale_elements,
+                (unsigned long long)sdiag.static_scale_first_block_mismatches,
+                (unsigned long long)sdiag.static_scale_later_block_mismatches);
+
+    // Reference-API carriers: head slices, strided views, owning matrices.
+    const sageattn::MatView<float> head = in.q.slice(B - 1, H - 1);
+    const sageattn::MatView<float> tail = head.block(N / 2, N - N / 2);
+    sageattn::Matrix<float> copy(tail.rows, tail.cols);
+    for (int r = 0; r < tail.rows; ++r)
+        for (int c = 0; c < tail.cols; ++c) copy(r, c) = tail(r, c);
+    const sageattn::MatView<float> cv(copy);
+    bool carriers = head.rows == N && head.cols == D && head.stride == D && tail.row(0).size() == size_t(D) &&
+                    cv(0, 0) == in.q.at(B - 1, H - 1, N / 2, 0) && copy == copy &&
+                    &head(0, 0) == in.q.slice_ptr(B - 1, H - 1);
+    std::printf(carriers ? "CARRIERS OK\n" : "CARRIERS FAILED\n");
+    // The exact oracle and the fp32 tiled baseline keep working through this header.
+    if (N <= 1024) {
+        const sageattn::Tensor4d exact = sageattn::naive_attention(in);
+        const sageattn::Tensor4f flash = sageattn::flash_attention_fp(in);
+        double dot = 0, na = 0, nb = 0, fmax = 0;
+        for (size_t i = 0; i < out.size(); ++i) {
+            dot += double(out.data[i]) * exact.data[i];
+            na += double(out.data[i]) * out.data[i];
+            nb += exact.data[i] * exact.data[i];
+            fmax = std::max(fmax, std::abs(double(flash.data[i]) - exact.data[i]));
+        }
+        std::printf("EXACT cos %.9f flash_maxerr %.3e\n", dot / std::sqrt(na * nb), fmax);
+    }
 
     bool ok = true;
     sageattn::KernelConfig bad = sageattn::kernel_config_for(sageattn::SageVariant::B);

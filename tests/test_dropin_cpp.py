@@ -31,6 +31,11 @@ def test_dropin_header_compiles_and_links(tmp_path):
 @pytest.mark.gpu
 @pytest.mark.parametrize("shape,causal", [((1, 2, 1024, 64), False), ((2, 1, 300, 128), True)])
 def test_dropin_runs_on_b200(tmp_path, cuda, oracle, shape, causal):
+    from oracle.oracle import Reference
+    try:
+        reference = Reference()
+    except (FileNotFoundError, OSError):
+        reference = None
     exe = _build(tmp_path)
     b, h, n, d = shape
     q, k, v = synth.qkv(b * h, n, d, dtype=np.float32, dist="outlier")
@@ -51,6 +56,17 @@ def test_dropin_runs_on_b200(tmp_path, cuda, oracle, shape, causal):
     assert cosine_sim(o, ref) >= 0.9999 and relative_l1(o, ref) <= 2e-3
     s, p = (int(x) for x in r.stdout.split("MACS")[1].split()[:2])
     assert (s, p) == tuple(int(x) for x in macs)
+    assert "CARRIERS OK" in r.stdout
+    cos = float(r.stdout.split("EXACT cos")[1].split()[0])
+    flash_err = float(r.stdout.split("flash_maxerr")[1].split()[0])
+    assert cos >= 0.999 and flash_err < 1e-4, (cos, flash_err)
+    # Static-scale diagnostics (attention.hpp:479-488): GPU counts vs the reference's.
+    el, first, later = (int(x) for x in r.stdout.split("STATIC")[1].split()[:3])
+    if reference is not None:
+        r_el, r_first, r_later = reference.static_scale_counts(q.reshape(shape), k.reshape(shape), v.reshape(shape),
+                                                               causal)
+        assert el == r_el
+        assert abs(first - r_first) <= max(2, 0.01 * r_first) and abs(later - r_later) <= max(2, 0.01 * r_later)
     o_t = np.fromfile(str(out) + ".t", np.float32).reshape(b * h, n, d)
     ref_t, _ = oracle.sage(q, k, v, causal, pv_fp32=True, per_token=True)
     assert cosine_sim(o_t, ref_t) >= 0.9999 and relative_l1(o_t, ref_t) <= 2e-3

@@ -245,3 +245,18 @@ def test_many_units_host_path_and_device_limit(cuda, oracle):
     qd, kd, vd = _to_dev([q, k, v], torch.float16, cuda)
     with pytest.raises(ValueError, match="65535"):
         sage_attention_cuda(qd, kd, vd)
+
+
+def test_host_path_pageable_and_pinned_agree(cuda):
+    """Pageable caller buffers are staged through pinned chunks (sab_capi.cu); pinned ones go
+    straight to cudaMemcpyAsync: both give the device path's output bit for bit."""
+    import torch
+
+    from paper_2410_02367_b200 import attention_fwd_host
+
+    q, k, v = (x.astype(np.float16) for x in _qkv(2, 24, 1000, 128))
+    o_page = attention_fwd_host(q, k, v, True, np.empty(q.shape, np.float32), devices=[0])
+    pq, pk, pv = (torch.from_numpy(x).pin_memory().numpy() for x in (q, k, v))
+    po = torch.empty(q.shape, dtype=torch.float32).pin_memory().numpy()
+    attention_fwd_host(pq, pk, pv, True, po, devices=[0])
+    assert np.array_equal(o_page, po)

@@ -138,3 +138,51 @@ def test_vb_against_reference_fixtures(cuda, path):
     o, ref = o.cpu().numpy().reshape(-1, n, d), g["o_vt"].reshape(-1, n, d)
     cs, rl = cosine_sim(o, ref), relative_l1(o, ref)
     assert cs >= COS_MIN and rl <= REL_L1_MAX, ("vT", cs, rl)
+
+
+@pytest.mark.parametrize("per_token", [False, True])
+@pytest.mark.parametrize("heads,n,d", [(35, 1024, 64), (79, 512, 128)])
+def test_host_path_short_last_chunk_int8_pv(cuda, per_token, heads, n, d):
+    """Host path with a short last unit chunk (35 units -> chunks of 4, last 3) on the INT8 P~V path:
+    every chunk keeps the full-chunk workspace layout, so V^ / delta_V never overlay the status
+    word -- the output equals the one-call device path bit for bit and no spurious error is raised."""
+    import torch
+
+    from paper_2410_02367_b200 import attention_fwd_host, sage_attention_cuda
+
+    q, k, v = (x.astype(np.float16) for x in _qkv(1, heads, n, d))
+    oh = attention_fwd_host(q, k, v, True, np.empty(q.shape, np.float32), devices=[0], per_token=per_token,
+                            pv_int8=True)
+    qd, kd, vd = (torch.from_numpy(x).to(cuda) for x in (q, k, v))
+    od = sage_attention_cuda(qd, kd, vd, causal=True, out_dtype=torch.float32, per_token=per_token, pv_int8=True)
+    assert np.array_equal(oh, od.cpu().numpy())
+
+
+def test_int8_pv_token_limit(cuda):
+    """The INT32 P~V accumulator bound: more than 133144 keys are refused on vB / vT (ValueError)."""
+    from paper_2410_02367_b200 import _lib
+
+    d = _lib.desc(1, 1, 133145, 64, pv_int8=True)
+    with pytest.raises(_lib.SabError, match="133144"):
+        _lib.check(_lib.load().sab_check_desc(d))
+    _lib.check(_lib.load().sab_check_desc(_lib.desc(1, 1, 133144, 64, pv_int8=True)))
+
+
+@pytest.mark.parametrize("causal,per_token", [(False, False), (True, False), (True, True)])
+def test_static_scale_diagnostics(cuda, reference, causal, per_token):
+    """SageDiagnostics::measure_static_scale on vB / vT (attention.hpp:479-488): the element count
+    equals the reference's, the mismatch counts agree with it to 1 % (the GPU's P~ differs from the
+    reference's by exponential ulps, which can move a code across a rounding boundary)."""
+    from paper_2410_02367_b200.sageattn import (AttentionInput, SageDiagnostics, SageOptions, SageVariant,
+                                                sage_attention)
+
+    b, h, n, d = 1, 3, 700, 64
+    q, k, v = _qkv(b, h, n, d)
+    diag = SageDiagnostics(measure_static_scale=True)
+    sage_attention(AttentionInput(q, k, v, causal), SageVariant.VT if per_token else SageVariant.VB,
+                   SageOptions(diagnostics=diag))
+    el, first, later = reference.static_scale_counts(q, k, v, causal, per_token)
+    assert diag.static_scale_elements == el
+    assert abs(diag.static_scale_first_block_mismatches - first) <= max(2, 0.01 * first)
+    assert abs(diag.static_scale_later_block_mismatches - later) <= max(2, 0.01 * later)
+    assert later > 0  # static scales do differ from per-token ones after the first block
