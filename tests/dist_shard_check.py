@@ -7,6 +7,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def main():
@@ -14,7 +15,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2410_02367_b200 import _lib
-    from tests.test_gpu_configs import _inputs, _run_as_benched
+    from gpu_helpers import _inputs, _run_as_benched
 
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()

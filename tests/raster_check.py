@@ -10,13 +10,14 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
 def main():
     import torch
 
     from oracle.oracle import Oracle, cosine_sim, relative_l1
-    from tests.test_gpu_configs import _inputs, _run_as_benched
+    from gpu_helpers import _inputs, _run_as_benched
 
     assert os.environ.get("SAB_L2_GROUP_MB") == "1"
     dev = torch.device("cuda:0")
