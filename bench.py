@@ -387,6 +387,9 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="strong (default): the workload as given, head x batch sharded over the ranks; "
                          "weak: N ranks run N x the workload's batch (fixed units per GPU)")
+    ap.add_argument("--shard-of", type=int, default=None,
+                    help="1-GPU strong-scaling probe: time rank 0's K3 shard of an N-GPU run of the workload "
+                         "(e.g. --workload C2 --shard-of 8 = the 4 units one GPU holds at 8 GPUs)")
     args = ap.parse_args()
     wl = workload(args.workload)
 
@@ -456,6 +459,11 @@ def main():
             dist.init_process_group("gloo")
             red_dev = torch.device("cpu")
     first, count = _lib.shard_plan(units_total, world, rank)
+    if args.shard_of and world == 1:
+        first, count = _lib.shard_plan(units_total, args.shard_of, 0)
+        total_ops = paper_ops(count, n, d, causal)
+        config["shard_of"] = {"gpus": args.shard_of, "rank": 0, "first_unit": first, "units": count,
+                              "note": "value is this shard's paper-OPS / its step time on one GPU"}
 
     q, k, v = device_inputs(count, n, d, first, dev)
     data = ("synthetic N(0,1) fp16 from the seeded counter RNG (global index; synth.tensor_torch, generated on "
@@ -463,6 +471,9 @@ def main():
     o = torch.empty_like(q)
     desc = sageattn.make_desc(q, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8)
     ws = sageattn.Workspace(desc, dev)
+    lay = _lib.SabWsLayout()
+    _lib.check(_lib.load().sab_workspace_layout(ctypes.byref(desc), ctypes.byref(lay)))
+    config["kv_split"] = {"kv_chunk_tiles": lay.kv_chunk, "chunks": lay.kv_nchunk} if lay.kv_chunk else "off"
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
@@ -598,8 +609,8 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int8 QK^T (s32 acc) / fp16 PV (fp32 acc); fp16 Q/K/V/O",
         "data": data, "config": config,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * units_total * n * d * 2,
-                "d2h_bytes_per_step": units_total * n * d * 2,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 3 * (count if args.shard_of else units_total) * n * d * 2,
+                "d2h_bytes_per_step": (count if args.shard_of else units_total) * n * d * 2,
                 "how": "sab_attention_fwd_host on pinned host fp16 buffers, fp16 O; wall clock, max over ranks"},
         # k1_mean_and_q (+ fused tree top) + k1_k_fast + k2_attention; vB adds k1_v_amax + k1_v_quant
         "gpu_launches": args.steps * (5 if pv_int8 else 3) * len(groups),

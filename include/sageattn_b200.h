@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SAB_ABI_VERSION 4
+#define SAB_ABI_VERSION 5
 
 /* Status codes.  The C++ shim maps them back to the reference's exceptions:
  * SAB_ERR_SHAPE / SAB_ERR_NONFINITE / SAB_ERR_UNSUPPORTED -> std::invalid_argument,
@@ -107,6 +107,18 @@ typedef struct sab_ws_layout {
                            channel max |v| scratch (INT8 P~V path only)              */
     uint64_t diag;      /* uint64 [2] static-scale mismatches (first KV block, later
                            blocks); zeroed by sab_prepass (ABI 4)                     */
+    /* KV-split plan (ABI 5): when the call has too few (unit, query-tile pair) items to
+     * fill the 148 SMs evenly (few heads per device under K3 sharding, long causal rows),
+     * K2 splits each pair's KV range into chunks of kv_chunk 64-key tiles; each chunk
+     * writes an unnormalised partial and the last chunk of a pair to finish merges them
+     * (the reference's q-block independence, attention.hpp:383).  kv_chunk == 0: no split
+     * and the three regions below are empty. */
+    uint64_t split_o;   /* float4 [units][pairs][kv_nchunk][head_dim/4][256] partial O  */
+    uint64_t split_ml;  /* float2 [units][pairs][kv_nchunk][256] (row max m, row sum l) */
+    uint64_t split_cnt; /* int32 [units][pairs][2] chunks finished / partials written
+                           (self-resetting)                                           */
+    int32_t kv_chunk;   /* 64-key tiles per chunk, 0 = no split                         */
+    int32_t kv_nchunk;  /* chunks of the longest pair (K2's grid.y)                      */
 } sab_ws_layout;
 
 const char* sab_status_string(int status);

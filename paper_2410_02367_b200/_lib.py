@@ -49,7 +49,8 @@ class SabWsLayout(C.Structure):
     _fields_ = [(name, C.c_uint64) for name in (
         "qcodes", "kcodes", "qscales", "kscales", "mean_k", "partials", "v16", "status", "total")] + [
         ("n_partials", C.c_int32), ("tree_depth", C.c_int32), ("vcodes", C.c_uint64), ("vscales", C.c_uint64),
-        ("diag", C.c_uint64)]
+        ("diag", C.c_uint64), ("split_o", C.c_uint64), ("split_ml", C.c_uint64), ("split_cnt", C.c_uint64),
+        ("kv_chunk", C.c_int32), ("kv_nchunk", C.c_int32)]
 
 
 class SabError(RuntimeError):

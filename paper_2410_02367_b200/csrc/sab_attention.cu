@@ -42,6 +42,7 @@
 // exact in real arithmetic because l and O share the stale max.
 #include <cuda.h>
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cuda_fp16.h>
 
@@ -172,7 +173,12 @@ struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
     uint64_t kv_full[16], kv_empty[16];
     uint64_t s_full[2][3], p_full[2][3], pv_done[2][3], o_final[2];
     uint32_t tmem_base;
+    int split_last;  // KV split: this CTA finished its pair's last chunk and merges
 };
+
+__device__ __forceinline__ void softmax_bar_sync() {  // the 16 softmax warps (threads 0-511)
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+}
 
 // Opaque copy: stops the compiler from keeping the 128 per-key mask predicates
 // of pass 1 alive (in registers) until pass 2.
@@ -236,7 +242,9 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
     rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
     float alpha = 1.0f;
     if (rescale) {
-        alpha = ex2(m - m_new);
+        // A row with no visible key yet (a KV-split chunk right of a causal row) keeps
+        // m = -inf: nothing to rescale.
+        alpha = m_new == -INFINITY ? 1.0f : ex2(m - m_new);
         m = m_new;
     }
     if (trole >= 0) SAB_STAMP(trole, ttile, 6);
@@ -256,11 +264,15 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
         const int c = 2 * i;
         const f2 t = ffma2(f2{__uint_as_float(r[c]), __uint_as_float(r[c + 1])}, cg2, bg);
         f2 pp;
+#ifdef SAB_SK_NOEXP  // timing skeleton: no exponentials (wrong results)
+        pp = t;
+#else
         if ((c & 15) >= 16 - POLY) {  // part of the exponentials on the FMA pipe
             pp = exp2_poly2(t);
         } else {
             pp = f2{ex2(t.x), ex2(t.y)};
         }
+#endif
         if (MASK) {
             pp.x = (c >= lim2) ? 0.0f : pp.x;
             pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
@@ -443,7 +455,9 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
     rescale = __any_sync(0xffffffffu, m_new > m + kRescaleThreshold);
     float alpha = 1.0f;
     if (rescale) {
-        alpha = ex2(m - m_new);
+        // A row with no visible key yet (a KV-split chunk right of a causal row) keeps
+        // m = -inf: nothing to rescale.
+        alpha = m_new == -INFINITY ? 1.0f : ex2(m - m_new);
         m = m_new;
     }
     const float mref = (m == -INFINITY) ? 0.0f : m;
@@ -540,6 +554,152 @@ __device__ __forceinline__ float softmax_half_pt_i8(uint32_t (&r)[32], uint32_t 
     return alpha;
 }
 
+// KV tiles of query-tile pair `pair` (the longer, tile B, when it exists).
+__host__ __device__ __forceinline__ int pair_kv_tiles(int pair, int ntq, int ntk, bool causal) {
+    if (!causal) return ntk;
+    const bool has_b = 2 * pair + 1 < ntq;
+    return min(has_b ? 4 * pair + 4 : 4 * pair + 2, ntk);
+}
+
+// First pair whose KV range extends past tile t0 (pair_kv_tiles is nondecreasing in the
+// pair index; t0 is below the longest pair's count for every existing chunk).
+__host__ __device__ __forceinline__ int split_pmin(int t0, int npair, int ntq, int ntk, bool causal) {
+    if (!causal) return 0;
+    int pm = min(t0 / 4, npair - 1);
+    while (pm > 0 && pair_kv_tiles(pm - 1, ntq, ntk, true) > t0) --pm;
+    while (pm < npair - 1 && pair_kv_tiles(pm, ntq, ntk, true) <= t0) ++pm;
+    return pm;
+}
+
+// One softmax thread's 32 output values of row qi, columns [col, col + 32), to O.
+template <int D, bool OUT_F32>
+__device__ __forceinline__ void store_o32(const AttnParams& p, int unit, int qi, int col, const float (&v)[32]) {
+    const size_t off = (static_cast<size_t>(unit) * p.n + qi) * D + col;
+    if (OUT_F32) {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+    } else {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
+                                pack_half2(v[8 * e + 4], v[8 * e + 5]), pack_half2(v[8 * e + 6], v[8 * e + 7]));
+    }
+}
+
+// KV-split epilogue, run by the 16 softmax warps of every chunk CTA of a split pair
+// once the chunk's O is final in TMEM (FP16-P~V path only: the INT8 path never splits).
+// The pair's chunks count themselves in on a per-pair counter as they finish.  Every
+// chunk but the last writes its unnormalised O (against its own row max m, log2 units)
+// and (m, l) to the workspace, then bumps a second, "written" counter; the last one waits
+// for those writes (its peers are past their compute, so only stores are outstanding),
+// resets both counters and merges the peers' partials with its own O read from TMEM:
+//   M = max_s m_s,  O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s
+// (the online-softmax identity of attention.hpp:429-443 across chunks).  Partials are
+// stored column-group-major ([item][d/4][256 rows] float4) so a warp's accesses coalesce.
+template <int D, bool OUT_F32>
+__device__ __noinline__ void split_epilogue(const AttnParams& p, Bars* bars, uint32_t t_o, int unit, int pair,
+                                            int npair, int chunk, int nch, int x, int row, int half, int qi,
+                                            bool valid, float m, float l) {
+    const size_t pair_idx = static_cast<size_t>(unit) * npair + pair;
+    int* arrive = p.split_cnt + 2 * pair_idx;
+    int* written = arrive + 1;
+    const size_t item0 = pair_idx * p.nchunk;
+    const int r = x * kBM + row;
+    if (!valid || m == -INFINITY) {  // no key of this chunk is visible to the row
+        m = -INFINITY;
+        l = 0.0f;
+    }
+    softmax_bar_sync();  // both tiles' O are final
+    if (threadIdx.x == 0) bars->split_last = atomicAdd(arrive, 1) == nch - 1;
+    softmax_bar_sync();
+    const bool last = bars->split_last;
+    if (!last) {
+        if (half == 0) p.part_ml[(item0 + chunk) * 256 + r] = make_float2(m, l);
+        if (valid) {
+            float4* po = reinterpret_cast<float4*>(p.part_o) + (item0 + chunk) * (D / 4) * 256 + r;
+#pragma unroll 1
+            for (int c = 0; c < D / 2; c += 32) {
+                uint32_t o[32];
+                tmem_ld16x2_32o<D / 2>(t_o + c, o);
+                tmem_wait_ld();
+                const int g0 = (half * (D / 2) + c) / 4;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    po[(g0 + e) * 256] = make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
+                                                     __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
+            }
+        }
+        __threadfence();
+        softmax_bar_sync();
+        if (threadIdx.x == 0) atomicAdd(written, 1);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        while (atomicAdd(written, 0) < nch - 1) __nanosleep(32);
+        *arrive = 0;  // ready for the next call
+        *written = 0;
+        __threadfence();
+    }
+    softmax_bar_sync();
+    // Every term is accumulated in chunk order, the CTA's own chunk in its place, so the
+    // result is bit-identical whichever chunk finishes last.
+    float mm = m;
+    for (int s = 0; s < nch; ++s)
+        if (s != chunk) mm = fmaxf(mm, __ldcg(&p.part_ml[(item0 + s) * 256 + r]).x);
+    float lsum = 0.0f;
+    for (int s = 0; s < nch; ++s) {
+        const float2 ml = s == chunk ? make_float2(m, l) : __ldcg(&p.part_ml[(item0 + s) * 256 + r]);
+        if (ml.x != -INFINITY) lsum += ex2(ml.x - mm) * ml.y;
+    }
+    const float inv_l = 1.0f / lsum;
+    bool finite = true;
+#pragma unroll 1
+    for (int c = 0; c < D / 2; c += 32) {
+        uint32_t own[32];
+        if (valid) {
+            tmem_ld16x2_32o<D / 2>(t_o + c, own);
+            tmem_wait_ld();
+        }
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+        const int g0 = (half * (D / 2) + c) / 4;
+#pragma unroll 1
+        for (int s = 0; s < nch; ++s) {
+            const float2 ml = s == chunk ? make_float2(m, l) : __ldcg(&p.part_ml[(item0 + s) * 256 + r]);
+            if (ml.x == -INFINITY) continue;  // no key of chunk s is visible to the row
+            const float w = ex2(ml.x - mm);
+            float4 t[8];
+            if (s == chunk) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    t[e] = make_float4(__uint_as_float(own[4 * e]), __uint_as_float(own[4 * e + 1]),
+                                       __uint_as_float(own[4 * e + 2]), __uint_as_float(own[4 * e + 3]));
+            } else {
+                const float4* src = reinterpret_cast<const float4*>(p.part_o) + (item0 + s) * (D / 4) * 256 + r;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) t[e] = __ldcg(src + (g0 + e) * 256);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                v[4 * e] = fmaf(w, t[e].x, v[4 * e]);
+                v[4 * e + 1] = fmaf(w, t[e].y, v[4 * e + 1]);
+                v[4 * e + 2] = fmaf(w, t[e].z, v[4 * e + 2]);
+                v[4 * e + 3] = fmaf(w, t[e].w, v[4 * e + 3]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            v[e] *= inv_l;
+            finite &= isfinite(v[e]);
+        }
+        if (qi < p.n) store_o32<D, OUT_F32>(p, unit, qi, half * (D / 2) + c, v);
+    }
+    if (qi < p.n && !finite) atomicOr(p.status, kStatusOverflow);
+}
+
 template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -566,10 +726,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ntk = (n + kBN - 1) / kBN;
     const int npair = (ntq + 1) / 2;
 
-    int unit, pair;
+    int unit, pair, chunk = 0;
     if (DUMP) {
         unit = p.dump_unit;
         pair = p.dump_qtile / 2;
+    } else if (p.kv_chunk > 0) {
+        // KV split: items are enumerated chunk-major, longest pairs first inside a chunk.
+        // Pair work (KV tiles) is nondecreasing in the pair index, so chunk c exists for
+        // pairs [split_pmin(c), npair) -- no empty CTAs, no item table.
+        int idx = static_cast<int>(blockIdx.x);
+        for (;; ++chunk) {
+            const int cnt = (npair - split_pmin(chunk * p.kv_chunk, npair, ntq, ntk, CAUSAL)) * p.units;
+            if (idx < cnt) break;
+            idx -= cnt;
+        }
+        unit = idx % p.units;
+        pair = npair - 1 - idx / p.units;
     } else {
         // Raster: units are taken in groups whose K^/V fit in L2 together (group_units,
         // chosen by the host), so each K^/V tile is fetched from HBM about once and
@@ -585,8 +757,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qt0 = 2 * pair;
     const bool has_b = qt0 + 1 < ntq;
     // Causal: query tile qt (rows < 128(qt+1)) needs KV tiles j with 64j <= 128qt + 127.
-    const int nkv_a = CAUSAL ? min(2 * qt0 + 2, ntk) : ntk;
-    const int nkv_b = has_b ? (CAUSAL ? min(2 * qt0 + 4, ntk) : ntk) : 0;
+    int nkv_a = CAUSAL ? min(2 * qt0 + 2, ntk) : ntk;
+    int nkv_b = has_b ? (CAUSAL ? min(2 * qt0 + 4, ntk) : ntk) : 0;
+    // KV split (p.kv_chunk > 0, grid.y = chunk): this CTA covers the pair's KV tiles
+    // [j0, j0 + kv_chunk); pairs with a single chunk run the unsplit epilogue.  Below,
+    // j counts tiles from j0 (ring stages, barrier phases); kb / TMA coordinates use j0 + j.
+    int j0 = 0, nch = 1;
+    if (!DUMP && p.kv_chunk > 0) {
+        const int nkv_full = max(nkv_a, nkv_b);
+        nch = (nkv_full + p.kv_chunk - 1) / p.kv_chunk;
+        j0 = chunk * p.kv_chunk;
+        const int j1 = min(nkv_full, j0 + p.kv_chunk);
+        nkv_a = max(0, min(nkv_a, j1) - j0);
+        nkv_b = max(0, min(nkv_b, j1) - j0);
+    }
     const int nkv = max(nkv_a, nkv_b);
 
     {  // constant operands of the bias MMA, written once through the generic proxy
@@ -636,14 +820,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(smem_u32(&bars->kv_empty[s]), ph ^ 1);
                 SAB_STAMP(4, j, 1);
                 const uint32_t full = smem_u32(&bars->kv_full[s]);
+#ifdef SAB_SK_NOKV  // timing skeleton: K^/V loaded for the first ring fill only (wrong results)
+                if (j >= S) {
+                    mbar_arrive(full);
+                    continue;
+                }
+#endif
                 mbar_arrive_expect_tx(full, C::kKBytes + (VI8 ? kBN * D : C::kVBytes));
-                tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, j * kBN, unit);
+                const int key0 = (j0 + j) * kBN;
+                tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, key0, unit);
                 if (VI8) {  // V^ transposed: D channel rows of 64 key codes (K-major B operand)
-                    tma_load_3d(sV + s * C::kVBytes, &tm_v, full, j * kBN, 0, unit);
+                    tma_load_3d(sV + s * C::kVBytes, &tm_v, full, key0, 0, unit);
                 } else {
 #pragma unroll
                     for (int c = 0; c < D / 64; ++c)
-                        tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, j * kBN, unit);
+                        tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, key0, unit);
                 }
             }
         }
@@ -676,11 +867,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // Bias MMA: S = 2^23 + 2^22 as binary32 (bits 0x4B400000) from constant fp16
                 // operands, then the INT32 QK^T products accumulate onto those bits, so the
                 // softmax reads float(2^23 + 2^22 + acc) directly.
+#ifndef SAB_SK_NOBIAS  // timing skeleton: no bias MMA (wrong results)
                 umma_f16_ss(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
+#endif
 #pragma unroll
                 for (int kk = 0; kk < D / 32; ++kk)
                     umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2), idesc_qk,
+#ifdef SAB_SK_NOBIAS
+                               kk > 0 ? 1u : 0u);
+#else
                                1u);
+#endif
                 umma_commit(smem_u32(&bars->s_full[x][j % NB]));
             }
             __syncwarp();
@@ -757,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  : p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
             const float* ksc = p.kscales + static_cast<size_t>(unit) * (PT ? npad : ntk);
             // The K scale of the next KV tile is fetched one iteration ahead.
-            float ks_next = PT ? 0.0f : __ldg(ksc);
+            float ks_next = PT ? 0.0f : __ldg(ksc + j0);
             const bool tr = (warp % 8) == 0 && lane == 0;
             // Software pipeline: S(j+1) is loaded from TMEM while P(j) is stored and
             // handed to the MMA issuer, so the load latency is off the per-tile chain.
@@ -769,7 +966,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll(PT ? 1 : 2)  // B: compile-time buffer parity per copy (+1-2 %); T would spill
             for (int j = 0; j < nkv_x; ++j) {
                 const float ks_cur = ks_next;
-                if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + j + 1);
+                if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + j0 + j + 1);
                 const int b = j % NB;
                 tmem_wait_ld_dep(r);
                 if (tr) SAB_STAMP(x, j, 1);
@@ -777,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int32_t* dump = (DUMP && qt == p.dump_qtile)
                                     ? p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN + 32 * half
                                     : nullptr;
-                const int kb = j * kBN;
+                const int kb = (j0 + j) * kBN;
                 // Dequant factor of this 64-key group: dQ * dK * log2(e), so that p = 2^(s - m).
                 const float cg = qsl * ks_cur;
                 const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
@@ -787,9 +984,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* dkp = ksc + kb + 32 * half;
                     if (p.diag)  // static-scale diagnostics (rare, slow path)
                         alpha = need_mask ? softmax_half_pt_i8<true, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, qi, n, m,
-                                                                                   l, rescale, p.diag, j == 0)
+                                                                                   l, rescale, p.diag, j0 + j == 0)
                                           : softmax_half_pt_i8<false, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, qi, n,
-                                                                                    m, l, rescale, p.diag, j == 0);
+                                                                                    m, l, rescale, p.diag, j0 + j == 0);
                     else if (need_mask)
                         alpha = softmax_half_pt_i8<true, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale,
                                                                         nullptr, false);
@@ -799,9 +996,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else if (VI8) {
                     if (p.diag)
                         alpha = need_mask ? softmax_half_i8<true, CAUSAL, true>(r, t_s, half, cg, kb, qi, n, m, l,
-                                                                                rescale, p.diag, j == 0)
+                                                                                rescale, p.diag, j0 + j == 0)
                                           : softmax_half_i8<false, CAUSAL, true>(r, t_s, half, cg, kb, qi, n, m, l,
-                                                                                 rescale, p.diag, j == 0);
+                                                                                 rescale, p.diag, j0 + j == 0);
                     else if (need_mask)
                         alpha = softmax_half_i8<true, CAUSAL, false>(r, t_s, half, cg, kb, qi, n, m, l, rescale,
                                                                      nullptr, false);
@@ -867,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(smem_u32(&bars->o_final[x]), 0);
             tc_fence_after();
             l += __shfl_xor_sync(0xffffffffu, l, 16);  // the two column halves of the row
-            if (!DUMP) {
+            if (!DUMP && nch == 1) {  // (KV-split chunks: split_epilogue below)
                 const float inv_l = 1.0f / l;
                 bool finite = true;
 #pragma unroll 1
@@ -897,26 +1094,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             v[e] = __uint_as_float(o[e]) * inv_l;
                         }
                     }
-                    if (qi < n) {
-                        const size_t off = (static_cast<size_t>(unit) * n + qi) * D + half * (D / 2) + c;
-                        if (OUT_F32) {
-                            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
-#pragma unroll
-                            for (int e = 0; e < 8; ++e)
-                                dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                        } else {
-                            uint4* dst = reinterpret_cast<uint4*>(static_cast<__half*>(p.o) + off);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                dst[e] = make_uint4(pack_half2(v[8 * e], v[8 * e + 1]), pack_half2(v[8 * e + 2], v[8 * e + 3]),
-                                                    pack_half2(v[8 * e + 4], v[8 * e + 5]),
-                                                    pack_half2(v[8 * e + 6], v[8 * e + 7]));
-                        }
-                    }
+                    if (qi < n) store_o32<D, OUT_F32>(p, unit, qi, half * (D / 2) + c, v);
                 }
                 if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
             }
         }
+        if (!DUMP && !VI8 && nch > 1)
+            split_epilogue<D, OUT_F32>(p, bars, t_o, unit, pair, npair, chunk, nch, x, row, half, qi, nkv_x > 0, m, l);
     }
 
     tc_fence_before();
@@ -990,7 +1174,14 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int ntq = (p.n + kBM - 1) / kBM;
-    const unsigned grid = DUMP ? 1u : static_cast<unsigned>((ntq + 1) / 2) * static_cast<unsigned>(p.units);
+    const int npair = (ntq + 1) / 2, ntk = (p.n + kBN - 1) / kBN;
+    unsigned grid = DUMP ? 1u : static_cast<unsigned>(npair) * static_cast<unsigned>(p.units);
+    if (!DUMP && p.kv_chunk > 0) {  // one CTA per (unit, pair, chunk) item
+        long long items = 0;
+        for (int c = 0; c < p.nchunk; ++c)
+            items += static_cast<long long>(npair - split_pmin(c * p.kv_chunk, npair, ntq, ntk, CAUSAL)) * p.units;
+        grid = static_cast<unsigned>(items);
+    }
 #ifdef SAB_TRACE
     cudaMemcpyToSymbolAsync(g_trace, &h_trace_ptr, sizeof(h_trace_ptr), 0, cudaMemcpyHostToDevice, s);
     cudaMemcpyToSymbolAsync(g_trace_cta, &h_trace_cta, sizeof(int), 0, cudaMemcpyHostToDevice, s);
@@ -1024,6 +1215,53 @@ cudaError_t dispatch(const AttnParams& p, cudaStream_t s) {
 }
 
 }  // namespace
+
+// KV-split plan.  K2 runs one CTA per (unit, query-tile pair); a pair's work is its KV
+// tile count (all ntk tiles, or min(4p+4, ntk) when causal).  When the longest pair is
+// well above the average work per SM -- few units per device under K3 sharding (C2 on
+// 8 GPUs: 4 units = 128 CTAs, longest pair 128 tiles vs 57 per SM), or short sequences --
+// the block scheduler cannot balance the grid, so pairs longer than about the per-SM
+// work are cut into chunks of that length (at least 16 tiles, at most 32 chunks).
+// SAB_KV_SPLIT=<tiles> forces a chunk length (tests), SAB_KV_SPLIT=0 disables the split.
+void kv_split_plan(int64_t units, int n, int causal, int* kv_chunk, int* nchunk) {
+    static const int forced = [] {
+        const char* e = std::getenv("SAB_KV_SPLIT");
+        return e ? std::atoi(e) : -1;
+    }();
+    constexpr int kSms = 148;  // B200
+    *kv_chunk = 0;
+    *nchunk = 1;
+    if (forced == 0 || units < 1 || n < 1) return;
+    const int ntq = (n + kBM - 1) / kBM, ntk = (n + kBN - 1) / kBN, npair = (ntq + 1) / 2;
+    int64_t per_unit = 0;
+    int longest = 0;
+    for (int pr = 0; pr < npair; ++pr) {
+        const int len = pair_kv_tiles(pr, ntq, ntk, causal != 0);
+        per_unit += len;
+        longest = std::max(longest, len);
+    }
+    const double per_sm = static_cast<double>(per_unit) * static_cast<double>(units) / kSms;
+    int len;
+    if (forced > 0) {
+        len = forced;
+    } else {
+        // Cut the longest pairs to about the per-SM work: chunks cost a CTA prologue and a
+        // partial write each, so as few as balance needs (C2's 4-unit shard: 2 x 64 tiles).
+        if (longest <= 1.15 * per_sm) return;
+        const int nch = static_cast<int>(std::ceil(longest / std::max(16.0, 1.15 * per_sm)));
+        if (nch < 2) return;
+        len = (longest + nch - 1) / nch;
+    }
+    if (len >= longest) return;
+    int nch = (longest + len - 1) / len;
+    if (nch > 32) {
+        nch = 32;
+        len = (longest + 31) / 32;
+        nch = (longest + len - 1) / len;
+    }
+    *kv_chunk = len;
+    *nchunk = nch;
+}
 
 cudaError_t launch_attention(const AttnParams& p, cudaStream_t s) { return dispatch<false>(p, s); }
 

@@ -65,6 +65,17 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     L->vcodes = take(pv8 ? units * hd * npad : 0);
     L->vscales = take(pv8 ? 2 * units * hd * sizeof(float) : 0);
     L->diag = take(2 * sizeof(unsigned long long));
+    int kv_chunk = 0, nchunk = 1;
+    // The INT8 P~V path quantizes P~ against the running row max (quantize_p_static,
+    // quant.hpp:258-279), so chunked maxima would change its codes: no split there.
+    if (!pv8) kv_split_plan(int64_t(units), d->tokens, d->causal, &kv_chunk, &nchunk);
+    const size_t npair = (size_t(d->tokens) + 2 * kBlockQ - 1) / (2 * kBlockQ);
+    const size_t items = kv_chunk ? units * npair * size_t(nchunk) : 0;
+    L->split_o = take(items * 2 * kBlockQ * hd * sizeof(float));
+    L->split_ml = take(items * 2 * kBlockQ * 2 * sizeof(float));
+    L->split_cnt = take(kv_chunk ? 2 * units * npair * sizeof(int32_t) : 0);
+    L->kv_chunk = kv_chunk;
+    L->kv_nchunk = kv_chunk ? nchunk : 0;
     L->total = off;
     L->n_partials = n_partials;
     L->tree_depth = depth;
@@ -136,10 +147,21 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
     a.out_f32 = d->out_dtype == SAB_F32;
     a.per_token = d->qk_granularity == SAB_QK_PER_TOKEN;
     a.diag = (pv8 && d->measure_static_scale) ? at<unsigned long long>(w, L.diag) : nullptr;
+    a.kv_chunk = L.kv_chunk;
+    a.nchunk = L.kv_chunk ? L.kv_nchunk : 1;
+    a.part_o = L.kv_chunk ? at<float>(w, L.split_o) : nullptr;
+    a.part_ml = L.kv_chunk ? at<float2>(w, L.split_ml) : nullptr;
+    a.split_cnt = L.kv_chunk ? at<int>(w, L.split_cnt) : nullptr;
     return a;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// The KV-split chunk counters are self-resetting; they are zeroed with the status word
+// so that a call aborted mid-kernel cannot leave a stale count behind.
+cudaError_t clear_split_counters(const sab_ws_layout& L, void* ws, cudaStream_t s) {
+    return cudaMemsetAsync(at<uint8_t>(ws, L.split_cnt), 0, size_t(L.total - L.split_cnt), s);
+}
 
 // K1's grid.y carries the unit index: one device call covers at most 65535 units (the
 // host-buffer path splits larger shards into chunks).
@@ -152,6 +174,7 @@ int enqueue_prepass(const sab_desc* d, const sab_ws_layout& L, const void* q, co
     if (reset) {
         cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t) * (1 + size_t(units_of(d))), s);
         if (e == cudaSuccess) e = cudaMemsetAsync(at<uint8_t>(ws, L.diag), 0, 2 * sizeof(unsigned long long), s);
+        if (e == cudaSuccess && L.kv_chunk) e = clear_split_counters(L, ws, s);
         if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: status reset");
     }
     cudaError_t e = launch_prepass(prepass_params(d, L, q, k, v, ws), s);
@@ -567,7 +590,8 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     uint8_t* ws = dout + out_bytes;
 
     if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t) * (1 + size_t(chunk)), ctx->s_cmp)) != cudaSuccess ||
-        (e = cudaMemsetAsync(ws + L.diag, 0, 2 * sizeof(unsigned long long), ctx->s_cmp)) != cudaSuccess)
+        (e = cudaMemsetAsync(ws + L.diag, 0, 2 * sizeof(unsigned long long), ctx->s_cmp)) != cudaSuccess ||
+        (L.kv_chunk && (e = clear_split_counters(L, ws, ctx->s_cmp)) != cudaSuccess))
         return cuda_fail(e, "sab_attention_fwd_host: memset");
     // Copies the finished O of chunk c out of its pinned slot into the caller's buffer.
     auto drain_out = [&](int c) -> cudaError_t {

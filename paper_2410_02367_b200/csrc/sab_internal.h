@@ -73,7 +73,17 @@ struct AttnParams {
     int dump_unit, dump_qtile;
     int group_units;  // K2 raster: units per L2-resident group (set by launch_attention)
     unsigned long long* diag;  // vB/vT static-scale P~ mismatches [first block, later blocks], or NULL
+    // KV split (sab_ws_layout::kv_chunk): chunk c of a pair covers KV tiles
+    // [c * kv_chunk, (c + 1) * kv_chunk); grid.y = nchunk.
+    int kv_chunk, nchunk;
+    float* part_o;          // [units][npair][nchunk][d/4][256] float4 groups of unnormalised partial O
+    float2* part_ml;        // [units][npair][nchunk][256] (m, l)
+    int* split_cnt;         // [units][npair][2] chunks finished / partials written (self-resetting)
 };
+
+// KV-split plan of one call (sab_ws_layout::kv_chunk / kv_nchunk): 0 / 1 when the
+// (unit, pair) items already spread evenly over the SMs.
+void kv_split_plan(int64_t units, int n, int causal, int* kv_chunk, int* nchunk);
 
 cudaError_t launch_attention(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_qk_dump(const AttnParams& p, cudaStream_t s);

@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sab_abi_version() == 4
+    assert lib.sab_abi_version() == 5
 
 
 def test_desc_validation_mirrors_reference():
