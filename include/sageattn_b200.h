@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SAB_ABI_VERSION 5
+#define SAB_ABI_VERSION 6
 
 /* Status codes.  The C++ shim maps them back to the reference's exceptions:
  * SAB_ERR_SHAPE / SAB_ERR_NONFINITE / SAB_ERR_UNSUPPORTED -> std::invalid_argument,
@@ -48,11 +48,12 @@ enum sab_status {
 
 enum sab_dtype { SAB_F16 = 0, SAB_F32 = 1 };
 
-/* PV accumulation.  SAB_PV_FP32 = FP32 accumulator in TMEM, the arm of
- * SageOptions::pv_fp32_accumulator (attention.hpp:75, 454-471).  SAB_PV_FP16_TILE
- * keeps the paper's FP16 accumulator per KV tile and flushes it into the
- * FP32 output. */
-enum sab_pv_accum { SAB_PV_FP32 = 0, SAB_PV_FP16_TILE = 1 };
+/* PV accumulation: FP32 accumulator in TMEM, the arm of
+ * SageOptions::pv_fp32_accumulator (attention.hpp:75, 454-471) -- the only one.
+ * The reference's default persistent-binary16 accumulator drifts by 4e-3..1.6e-2
+ * rel-L1 from its own FP32 arm, so no tensor-core accumulation order can
+ * reproduce it within the 2e-3 gate; any other value is rejected. */
+enum sab_pv_accum { SAB_PV_FP32 = 0 };
 
 /* Q/K scale granularity: KernelConfig::qk_granularity (attention.hpp:34, 41-46).
  * PER_BLOCK = SAGEAttn-B (128-token Q groups, 64-token K groups); PER_TOKEN =
@@ -141,6 +142,25 @@ int sab_workspace_layout(const sab_desc* d, sab_ws_layout* layout);
  * F16 and check_v is 0.  Resets and then sets the device status word. */
 int sab_prepass(const sab_desc* d, const void* q, const void* k, const void* v, void* ws, size_t ws_bytes,
                 void* stream);
+
+/* RoPE layouts of sab_prepass_rope: which channels form the rotated pairs. */
+enum sab_rope_layout {
+    SAB_ROPE_INTERLEAVED = 1, /* pairs (2i, 2i+1): GPT-J / the complex form          */
+    SAB_ROPE_HALF = 2         /* pairs (i, i + d/2): GPT-NeoX / rotate_half          */
+};
+
+/* K1 with the rotary position embedding fused into the quantizer -- the paper's
+ * "quantization fused into the RoPE kernel".  q and k are the
+ * PRE-rotation tensors; token t of every unit is rotated by cos/sin[t][i] (float
+ * [tokens][head_dim/2], device, 16-byte aligned) in binary32 with every product and
+ * sum rounded (no contraction):
+ *   x_a' = x_a*c - x_b*s,   x_b' = x_a*s + x_b*c     ((a, b) = the layout's pair i)
+ * and the result is exactly what sab_prepass would produce for the rotated tensors
+ * given as F32 inputs (mean(K) of the rotated K, fold, per-block / per-token codes).
+ * Same workspace and status contract as sab_prepass; K2 (sab_attention) is unchanged.
+ * ABI 6. */
+int sab_prepass_rope(const sab_desc* d, const void* q, const void* k, const void* v, const float* cos_table,
+                     const float* sin_table, int rope_layout, void* ws, size_t ws_bytes, void* stream);
 
 /* K2 -- replaces the q-block/kv-block engine of attention.hpp:383-541
  * (detail::int8_tile_nt, online softmax, P~V, normalize).  Reads Q^/K^/scales

@@ -79,7 +79,17 @@ class Oracle:
         lib.orc_quantize_int8_cols.argtypes = [_f32p, C.c_int, C.c_int, _i8p, _f32p]
         lib.orc_naive.argtypes = [_f32p, _f32p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
         lib.orc_naive_rows.argtypes = [_f32p, _f32p, _f32p] + [C.c_int] * 5 + [_f64p]
+        lib.orc_rope.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _f32p, _f32p, C.c_int]
         self.lib = lib
+
+    # -- RoPE (sab_prepass_rope's rotation, binary32 with every op rounded) ---------
+    def rope(self, x, cos, sin, layout):
+        """x (units, n, d) rotated by cos/sin (n, d/2); layout "interleaved" (pairs 2i, 2i+1)
+        or "half" (pairs i, i + d/2).  Returns a new float32 array."""
+        x = np.array(_f32(x), dtype=np.float32, copy=True)
+        units, n, d = x.shape
+        self.lib.orc_rope(x, units, n, d, _f32(cos), _f32(sin), {"interleaved": 1, "half": 2}[layout])
+        return x
 
     # -- scalar numerics ------------------------------------------------
     def snap_half(self, x: float) -> float:

@@ -127,6 +127,32 @@ void orc_fold_q(const float* q, size_t count, int d, float* qf)
 }
 
 /* ------------------------------------------------------------------------ */
+/* RoPE (the product's sab_prepass_rope; PAPER.md:397 fuses quantization    */
+/* into the RoPE kernel).  The reference has no RoPE: this restates the      */
+/* rotation as sab_prepass_rope defines it -- binary32, every product and    */
+/* sum rounded -- so the fused K1 can be compared with                       */
+/* prepass(rope(q), rope(k)) bit for bit.  layout 1: pairs (2i, 2i+1);       */
+/* layout 2: pairs (i, i + d/2).  x' = x_a c - x_b s, x_b' = x_a s + x_b c.  */
+/* cs / sn: [n][d/2]; x: units x n x d, rotated in place.                   */
+/* ------------------------------------------------------------------------ */
+void orc_rope(float* x, int units, int n, int d, const float* cs, const float* sn, int layout)
+{
+    const int h = d / 2;
+    for (int u = 0; u < units; ++u)
+        for (int t = 0; t < n; ++t) {
+            float* row = x + ((size_t)u * n + t) * d;
+            for (int i = 0; i < h; ++i) {
+                const int a = layout == 1 ? 2 * i : i, b = layout == 1 ? 2 * i + 1 : i + h;
+                const float c = cs[(size_t)t * h + i], s = sn[(size_t)t * h + i];
+                const float xa = row[a], xb = row[b];
+                const float ac = xa * c, bs = xb * s, as = xa * s, bc = xb * c;
+                row[a] = ac - bs;
+                row[b] = as + bc;
+            }
+        }
+}
+
+/* ------------------------------------------------------------------------ */
 /* INT8 per-block dynamic quantizer (quant.hpp:95-173, INT8 arm only).      */
 /* ------------------------------------------------------------------------ */
 

@@ -24,11 +24,12 @@ SAB_ERR_ARGUMENT = 8
 SAB_F16 = 0
 SAB_F32 = 1
 SAB_PV_FP32 = 0
-SAB_PV_FP16_TILE = 1
 SAB_QK_PER_BLOCK = 0  # SAGEAttn-B
 SAB_QK_PER_TOKEN = 1  # SAGEAttn-T
 SAB_PV_PATH_FP16 = 0  # B / T
 SAB_PV_PATH_INT8 = 1  # vB
+SAB_ROPE_INTERLEAVED = 1  # pairs (2i, 2i+1)
+SAB_ROPE_HALF = 2  # pairs (i, i + d/2)
 
 # Every symbol include/sageattn_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
@@ -36,6 +37,7 @@ EXPORTS = (
     "sab_workspace_size", "sab_workspace_layout", "sab_prepass", "sab_attention", "sab_attention_fwd",
     "sab_read_status", "sab_attention_fwd_host", "sab_shard_plan", "sab_qk_int32_tiles", "sab_diagnostics",
     "sab_device_count", "sab_device_ordinals", "sab_attention_fwd_host_diag", "sab_read_static_scale_counts",
+    "sab_prepass_rope",
 )
 
 
@@ -95,6 +97,7 @@ def load():
     lib.sab_device_ordinals.argtypes = [P(C.c_int), C.c_int, P(C.c_int)]
     lib.sab_attention_fwd_host_diag.argtypes = [P(SabDesc), vp, vp, vp, vp, P(C.c_int), C.c_int, P(C.c_uint64)]
     lib.sab_read_static_scale_counts.argtypes = [P(SabDesc), vp, vp, P(C.c_uint64)]
+    lib.sab_prepass_rope.argtypes = [P(SabDesc), vp, vp, vp, vp, vp, C.c_int, vp, sz, vp]
     for name in EXPORTS:
         if name not in ("sab_desc_init", "sab_status_string", "sab_last_error"):
             getattr(lib, name).restype = C.c_int

@@ -61,19 +61,21 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     L->partials = take(units * size_t(n_partials) * hd * sizeof(float));
     const bool pv8 = d->pv_path == SAB_PV_PATH_INT8;
     L->v16 = take(d->in_dtype == SAB_F32 && !pv8 ? units * n * hd * 2 : 0);
-    L->status = take(sizeof(int32_t) * (1 + units));  // status word + per-unit K1 counters
-    L->vcodes = take(pv8 ? units * hd * npad : 0);
-    L->vscales = take(pv8 ? 2 * units * hd * sizeof(float) : 0);
-    L->diag = take(2 * sizeof(unsigned long long));
     int kv_chunk = 0, nchunk = 1;
     // The INT8 P~V path quantizes P~ against the running row max (quantize_p_static,
     // quant.hpp:258-279), so chunked maxima would change its codes: no split there.
     if (!pv8) kv_split_plan(int64_t(units), d->tokens, d->causal, &kv_chunk, &nchunk);
     const size_t npair = (size_t(d->tokens) + 2 * kBlockQ - 1) / (2 * kBlockQ);
     const size_t items = kv_chunk ? units * npair * size_t(nchunk) : 0;
+    // Everything a call must find zeroed is contiguous (one memset per call, see
+    // reset_bytes): status word + per-unit K1 counters, static-scale counters, split counters.
+    L->status = take(sizeof(int32_t) * (1 + units));
+    L->diag = take(2 * sizeof(unsigned long long));
+    L->split_cnt = take(kv_chunk ? 2 * units * npair * sizeof(int32_t) : 0);
+    L->vcodes = take(pv8 ? units * hd * npad : 0);
+    L->vscales = take(pv8 ? 2 * units * hd * sizeof(float) : 0);
     L->split_o = take(items * 2 * kBlockQ * hd * sizeof(float));
     L->split_ml = take(items * 2 * kBlockQ * 2 * sizeof(float));
-    L->split_cnt = take(kv_chunk ? 2 * units * npair * sizeof(int32_t) : 0);
     L->kv_chunk = kv_chunk;
     L->kv_nchunk = kv_chunk ? nchunk : 0;
     L->total = off;
@@ -157,10 +159,12 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// The KV-split chunk counters are self-resetting; they are zeroed with the status word
-// so that a call aborted mid-kernel cannot leave a stale count behind.
-cudaError_t clear_split_counters(const sab_ws_layout& L, void* ws, cudaStream_t s) {
-    return cudaMemsetAsync(at<uint8_t>(ws, L.split_cnt), 0, size_t(L.total - L.split_cnt), s);
+// Bytes from L.status that every call zeroes in one memset: the status word, K1's
+// per-unit counters, the static-scale counters and the KV-split counters (the counters
+// are self-resetting; zeroing them too means an aborted call leaves nothing stale).
+size_t reset_bytes(const sab_ws_layout& L) {
+    const size_t end = L.kv_chunk ? L.vcodes : L.split_cnt;  // split_cnt is empty without a split
+    return size_t(end - L.status);
 }
 
 // K1's grid.y carries the unit index: one device call covers at most 65535 units (the
@@ -172,9 +176,7 @@ int enqueue_prepass(const sab_desc* d, const sab_ws_layout& L, const void* q, co
     if (units_of(d) > kMaxUnitsPerLaunch)
         return set_error(SAB_ERR_UNSUPPORTED, "sab_prepass: batch*heads above 65535 per device call");
     if (reset) {
-        cudaError_t e = cudaMemsetAsync(at<int>(ws, L.status), 0, sizeof(int32_t) * (1 + size_t(units_of(d))), s);
-        if (e == cudaSuccess) e = cudaMemsetAsync(at<uint8_t>(ws, L.diag), 0, 2 * sizeof(unsigned long long), s);
-        if (e == cudaSuccess && L.kv_chunk) e = clear_split_counters(L, ws, s);
+        cudaError_t e = cudaMemsetAsync(at<uint8_t>(ws, L.status), 0, reset_bytes(L), s);
         if (e != cudaSuccess) return cuda_fail(e, "sab_prepass: status reset");
     }
     cudaError_t e = launch_prepass(prepass_params(d, L, q, k, v, ws), s);
@@ -303,6 +305,34 @@ int sab_prepass(const sab_desc* d, const void* q, const void* k, const void* v, 
     if (!aligned16(q) || !aligned16(k) || (v && !aligned16(v)) || !aligned16(ws))
         return set_error(SAB_ERR_ARGUMENT, "sab_prepass: pointers must be 16-byte aligned");
     return enqueue_prepass(d, L, q, k, v, ws, static_cast<cudaStream_t>(stream), true);
+}
+
+int sab_prepass_rope(const sab_desc* d, const void* q, const void* k, const void* v, const float* cos_table,
+                     const float* sin_table, int rope_layout, void* ws, size_t ws_bytes, void* stream) {
+    sab_ws_layout L;
+    int st = sab_workspace_layout(d, &L);
+    if (st) return st;
+    if (!q || !k || !cos_table || !sin_table) return set_error(SAB_ERR_ARGUMENT, "sab_prepass_rope: NULL pointer");
+    if (rope_layout != SAB_ROPE_INTERLEAVED && rope_layout != SAB_ROPE_HALF)
+        return set_error(SAB_ERR_ARGUMENT, "sab_prepass_rope: rope_layout must be SAB_ROPE_INTERLEAVED or SAB_ROPE_HALF");
+    if ((d->in_dtype == SAB_F32 || d->check_v || d->pv_path == SAB_PV_PATH_INT8) && !v)
+        return set_error(SAB_ERR_ARGUMENT, "sab_prepass_rope: v is NULL");
+    if (!ws || ws_bytes < L.total) return set_error(SAB_ERR_WORKSPACE, "sab_prepass_rope: workspace too small");
+    if (!aligned16(q) || !aligned16(k) || (v && !aligned16(v)) || !aligned16(ws) || !aligned16(cos_table) ||
+        !aligned16(sin_table))
+        return set_error(SAB_ERR_ARGUMENT, "sab_prepass_rope: pointers must be 16-byte aligned");
+    if (units_of(d) > kMaxUnitsPerLaunch)
+        return set_error(SAB_ERR_UNSUPPORTED, "sab_prepass: batch*heads above 65535 per device call");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(at<uint8_t>(ws, L.status), 0, reset_bytes(L), s);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_prepass_rope: status reset");
+    PrepassParams pp = prepass_params(d, L, q, k, v, ws);
+    pp.rope = rope_layout;
+    pp.rope_cos = cos_table;
+    pp.rope_sin = sin_table;
+    e = launch_prepass(pp, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sab_prepass_rope: launch");
+    return SAB_OK;
 }
 
 int sab_attention(const sab_desc* d, void* ws, size_t ws_bytes, const void* v, void* o, void* stream) {
@@ -589,9 +619,7 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     uint8_t* dout = ctx->buf + 3 * in_bytes;
     uint8_t* ws = dout + out_bytes;
 
-    if ((e = cudaMemsetAsync(ws + L.status, 0, sizeof(int32_t) * (1 + size_t(chunk)), ctx->s_cmp)) != cudaSuccess ||
-        (e = cudaMemsetAsync(ws + L.diag, 0, 2 * sizeof(unsigned long long), ctx->s_cmp)) != cudaSuccess ||
-        (L.kv_chunk && (e = clear_split_counters(L, ws, ctx->s_cmp)) != cudaSuccess))
+    if ((e = cudaMemsetAsync(ws + L.status, 0, reset_bytes(L), ctx->s_cmp)) != cudaSuccess)
         return cuda_fail(e, "sab_attention_fwd_host: memset");
     // Copies the finished O of chunk c out of its pinned slot into the caller's buffer.
     auto drain_out = [&](int c) -> cudaError_t {

@@ -48,6 +48,11 @@ struct PrepassParams {
     int in_f32;
     float inv_n;        // 1.0f / float(N)          (quant.hpp:228)
     float fold;         // float(1/sqrt(double(d)))  (quant.hpp:249)
+    // RoPE fused into the quantizer (sab_prepass_rope): Q and K are rotated
+    // in binary32 on load, before the smooth / fold / quantize.  0 = off.
+    int rope;           // SAB_ROPE_INTERLEAVED / SAB_ROPE_HALF
+    const float* rope_cos;  // [n][d/2] per token position and channel pair
+    const float* rope_sin;
 };
 
 // Mean-tree geometry for N tokens (quant.hpp:203-213): the smallest depth at

@@ -75,6 +75,51 @@ __device__ __forceinline__ void load8<float>(const float* src, float (&x)[8]) {
     x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
 
+// RoPE of the 8 channels [col, col + 8) of token t (sab_prepass_rope), binary32 with
+// every product and sum rounded (no contraction):
+//   interleaved (pairs 2i, 2i+1):  x0' = x0 c - x1 s,   x1' = x0 s + x1 c
+//   half split  (pairs i, i+d/2):  x_i' = x_i c - x_{i+d/2} s,   x_{i+d/2}' = x_{i+d/2} c + x_i s
+// with c = cos[t][i], s = sin[t][i]; `pr` holds channels col ^ (d/2) (half split only).
+template <int D>
+__device__ __forceinline__ void rope8(const PrepassParams& p, int t, int col, float (&x)[8], const float (&pr)[8]) {
+    const float* cs = p.rope_cos + static_cast<size_t>(t) * (D / 2);
+    const float* sn = p.rope_sin + static_cast<size_t>(t) * (D / 2);
+    if (p.rope == SAB_ROPE_INTERLEAVED) {
+        const float4 c = __ldg(reinterpret_cast<const float4*>(cs + col / 2));
+        const float4 s = __ldg(reinterpret_cast<const float4*>(sn + col / 2));
+        const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float x0 = x[2 * e], x1 = x[2 * e + 1];
+            x[2 * e] = __fsub_rn(__fmul_rn(x0, cc[e]), __fmul_rn(x1, ss[e]));
+            x[2 * e + 1] = __fadd_rn(__fmul_rn(x0, ss[e]), __fmul_rn(x1, cc[e]));
+        }
+    } else {
+        const bool lo = col < D / 2;
+        const int i0 = lo ? col : col - D / 2;
+        float cc[8], ss[8];
+        *reinterpret_cast<float4*>(cc) = __ldg(reinterpret_cast<const float4*>(cs + i0));
+        *reinterpret_cast<float4*>(cc + 4) = __ldg(reinterpret_cast<const float4*>(cs + i0) + 1);
+        *reinterpret_cast<float4*>(ss) = __ldg(reinterpret_cast<const float4*>(sn + i0));
+        *reinterpret_cast<float4*>(ss + 4) = __ldg(reinterpret_cast<const float4*>(sn + i0) + 1);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            x[e] = lo ? __fsub_rn(__fmul_rn(x[e], cc[e]), __fmul_rn(pr[e], ss[e]))
+                      : __fadd_rn(__fmul_rn(x[e], cc[e]), __fmul_rn(pr[e], ss[e]));
+    }
+}
+
+// load8 of row `row` (token t), rotated when RoPE is on.
+template <typename T, int D>
+__device__ __forceinline__ void load8_rope(const PrepassParams& p, const T* rowp, int t, int col, float (&x)[8]) {
+    load8<T>(rowp + col, x);
+    if (p.rope) {
+        float pr[8];
+        if (p.rope == SAB_ROPE_HALF) load8<T>(rowp + (col ^ (D / 2)), pr);
+        rope8<D>(p, t, col, x, pr);
+    }
+}
+
 // Raw 8-element vector as loaded (fp16: 16 B, fp32: 32 B), kept in registers
 // in its input format so K1 keeps Q and K of a 128-token chunk on chip.
 template <typename T>
@@ -152,6 +197,20 @@ __device__ __forceinline__ void seq_sum(const T* base, int t0, int t1, int col, 
 // sums of one unit as a perfect binary tree (binary-counter evaluation, left +
 // right), then mean = sum * (1.0f / N)  (quant.hpp:228, 235).  Channel c; the
 // partials of the other CTAs are read through L2 (__ldcg).
+// seq_sum of rotated rows (RoPE on): one row at a time.
+template <typename T, int D>
+__device__ __forceinline__ void seq_sum_rope(const PrepassParams& p, const T* base, int t0, int t1, int col,
+                                             float (&s)[8]) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s[e] = 0.0f;
+    for (int t = t0; t < t1; ++t) {
+        float x[8];
+        load8_rope<T, D>(p, base + static_cast<size_t>(t) * D, t, col, x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], x[e]);
+    }
+}
+
 template <int D>
 __device__ __forceinline__ void mean_top(const PrepassParams& p, int unit, int c) {
     const float* part = p.partials + static_cast<size_t>(unit) * p.n_partials * D + c;
@@ -193,12 +252,18 @@ __device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, i
             int a, b;
             leaf_range(node0 + g, p.depth, p.n, a, b);
             if (b - a <= 8) {
-                seq_sum<T, D>(base, a, b, cv * 8, ns[g]);
+                if (p.rope) seq_sum_rope<T, D>(p, base, a, b, cv * 8, ns[g]);
+                else seq_sum<T, D>(base, a, b, cv * 8, ns[g]);
             } else {  // 9-token leaf: (4) + (5)
                 float lo[8], hi[8];
                 const int mid = a + (b - a) / 2;
-                seq_sum<T, D>(base, a, mid, cv * 8, lo);
-                seq_sum<T, D>(base, mid, b, cv * 8, hi);
+                if (p.rope) {
+                    seq_sum_rope<T, D>(p, base, a, mid, cv * 8, lo);
+                    seq_sum_rope<T, D>(p, base, mid, b, cv * 8, hi);
+                } else {
+                    seq_sum<T, D>(base, a, mid, cv * 8, lo);
+                    seq_sum<T, D>(base, mid, b, cv * 8, hi);
+                }
 #pragma unroll
                 for (int i = 0; i < 8; ++i) ns[g][i] = __fadd_rn(lo[i], hi[i]);
             }
@@ -394,8 +459,8 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
             float q[8], k[8];
             float aq = 0.0f, ak = 0.0f;
             if (valid) {
-                load8<T>(sq + row * D + col, q);
-                load8<T>(sk + row * D + col, k);
+                load8_rope<T, D>(p, sq + row * D, r0 + row, col, q);
+                load8_rope<T, D>(p, sk + row * D, r0 + row, col, k);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     finite &= isfinite(q[e]) && isfinite(k[e]);
@@ -446,7 +511,7 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
         return;
     }
 
-    if constexpr (std::is_same<T, __half>::value) {
+    if constexpr (std::is_same<T, __half>::value) if (!p.rope) {
         // fp16 fast path.  Every thread keeps one 8-channel column block (CV divides
         // the thread count), so its eight K means live in registers.
         const int col = (tid % CV) * 8;
@@ -551,8 +616,8 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
         const int row = v / CV, col = (v % CV) * 8;
         if (row < rows) {
             float q[8], k[8];
-            load8<T>(sq + row * D + col, q);
-            load8<T>(sk + row * D + col, k);
+            load8_rope<T, D>(p, sq + row * D, r0 + row, col, q);
+            load8_rope<T, D>(p, sk + row * D, r0 + row, col, k);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 nan_probe = fmaf(q[e], 0.0f, nan_probe);  // NaN iff some input is inf or NaN
@@ -598,8 +663,8 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
         const int row = v / CV, col = (v % CV) * 8;
         if (row < rows) {
             float q[8], k[8];
-            load8<T>(sq + row * D + col, q);
-            load8<T>(sk + row * D + col, k);
+            load8_rope<T, D>(p, sq + row * D, r0 + row, col, q);
+            load8_rope<T, D>(p, sk + row * D, r0 + row, col, k);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 q[e] = __fmul_rn(q[e], p.fold);
@@ -922,7 +987,7 @@ cudaError_t launch_v(const PrepassParams& p, cudaStream_t s) {
 template <typename T, int D>
 cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
-    if (std::is_same<T, __half>::value && p.smooth && !p.per_token) {
+    if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope) {
         const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
         constexpr int smem = kBlockQ * D * 2;
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;

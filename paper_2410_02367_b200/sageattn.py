@@ -234,16 +234,37 @@ def make_desc(q, causal: bool, out_dtype=None, smooth_k: bool = True, check_v: b
                      per_token=per_token, pv_int8=pv_int8)
 
 
+ROPE_LAYOUTS = {"interleaved": _lib.SAB_ROPE_INTERLEAVED, "half": _lib.SAB_ROPE_HALF}
+
+
+def _enqueue_prepass(desc, q, k, v, ws, stream, rope):
+    """sab_prepass, or sab_prepass_rope when rope = (cos, sin, layout) is given: cos / sin float32
+    CUDA tensors (N, d/2) and layout "interleaved" (pairs 2i, 2i+1) or "half" (pairs i, i+d/2)."""
+    vptr = v.data_ptr() if v is not None else None
+    lib = _lib.load()
+    if rope is None:
+        return lib.sab_prepass(C.byref(desc), q.data_ptr(), k.data_ptr(), vptr, ws.ptr, ws.nbytes, _stream_ptr(stream))
+    cos, sin, layout = rope
+    torch = _torch()
+    n, d = q.shape[2], q.shape[3]
+    for t in (cos, sin):
+        if t.dtype != torch.float32 or tuple(t.shape) != (n, d // 2) or not t.is_contiguous() or t.device != q.device:
+            raise ValueError("rope tables must be contiguous float32 (tokens, head_dim/2) on the inputs' device")
+    if layout not in ROPE_LAYOUTS:
+        raise ValueError(f"rope layout must be one of {sorted(ROPE_LAYOUTS)}")
+    return lib.sab_prepass_rope(C.byref(desc), q.data_ptr(), k.data_ptr(), vptr, cos.data_ptr(), sin.data_ptr(),
+                                ROPE_LAYOUTS[layout], ws.ptr, ws.nbytes, _stream_ptr(stream))
+
+
 def prepass_cuda(q, k, v=None, smooth_k: bool = True, ws: Optional[Workspace] = None, stream=None,
-                 per_token: bool = False, pv_int8: bool = False) -> Workspace:
+                 per_token: bool = False, pv_int8: bool = False, rope=None) -> Workspace:
     """K1 on CUDA tensors (B,H,N,d) fp16/fp32; returns the workspace holding codes/scales/mean
-    (and, with pv_int8, the per-channel V^ of SAGEAttn-vB)."""
+    (and, with pv_int8, the per-channel V^ of SAGEAttn-vB).  rope = (cos, sin, layout) rotates
+    Q and K inside K1 first (sab_prepass_rope)."""
     desc = make_desc(q, False, smooth_k=smooth_k, per_token=per_token, pv_int8=pv_int8)
     ws = ws or Workspace(desc, q.device)
-    vptr = v.data_ptr() if v is not None else None
     try:
-        _lib.check(_lib.load().sab_prepass(C.byref(desc), q.data_ptr(), k.data_ptr(), vptr, ws.ptr, ws.nbytes,
-                                           _stream_ptr(stream)))
+        _lib.check(_enqueue_prepass(desc, q, k, v, ws, stream, rope))
     except _lib.SabError as e:
         _raise_for(e)
     return ws
@@ -276,11 +297,12 @@ def read_status(ws: Workspace, stream=None) -> int:
 
 def sage_attention_cuda(q, k, v, causal: bool = False, out=None, out_dtype=None, smooth_k: bool = True,
                         ws: Optional[Workspace] = None, stream=None, check: bool = True, per_token: bool = False,
-                        pv_int8: bool = False):
+                        pv_int8: bool = False, rope=None):
     """K1 + K2 on device-resident CUDA tensors (B,H,N,d); returns O (fp16 by default).
 
     With check=True the stream is synchronised and data-dependent errors raise
-    like the reference; with check=False the call stays fully asynchronous."""
+    like the reference; with check=False the call stays fully asynchronous.
+    rope = (cos, sin, layout): Q and K are the pre-rotation tensors, rotated inside K1."""
     torch = _torch()
     out_dtype = out_dtype or (out.dtype if out is not None else torch.float16)
     desc = make_desc(q, causal, out_dtype=out_dtype, smooth_k=smooth_k, per_token=per_token, pv_int8=pv_int8)
@@ -290,8 +312,13 @@ def sage_attention_cuda(q, k, v, causal: bool = False, out=None, out_dtype=None,
     if out is None:
         out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
     try:
-        _lib.check(_lib.load().sab_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                                 out.data_ptr(), ws.ptr, ws.nbytes, _stream_ptr(stream)))
+        if rope is None:
+            _lib.check(_lib.load().sab_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                     out.data_ptr(), ws.ptr, ws.nbytes, _stream_ptr(stream)))
+        else:
+            _lib.check(_enqueue_prepass(desc, q, k, v, ws, stream, rope))
+            _lib.check(_lib.load().sab_attention(C.byref(desc), ws.ptr, ws.nbytes, v.data_ptr(), out.data_ptr(),
+                                                 _stream_ptr(stream)))
         if check:
             _lib.check(read_status(ws, stream))
     except _lib.SabError as e:

@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sab_abi_version() == 5
+    assert lib.sab_abi_version() == 6
 
 
 def test_desc_validation_mirrors_reference():
@@ -33,7 +33,7 @@ def test_desc_validation_mirrors_reference():
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 0, 1024, 64))) == _lib.SAB_ERR_SHAPE
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 96))) == _lib.SAB_ERR_UNSUPPORTED
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, block_q=64))) == _lib.SAB_ERR_UNSUPPORTED
-    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=_lib.SAB_PV_FP16_TILE))) == \
+    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=1))) == \
         _lib.SAB_ERR_UNSUPPORTED
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, per_token=True))) == _lib.SAB_OK
     assert lib.sab_check_desc(C.byref(_lib.desc(2, 32768, 64, 64))) == _lib.SAB_OK  # host path chunks it
