@@ -1143,7 +1143,7 @@ bool make_map(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int ele
 
 // Raster groups: as few groups as keep each group's K^ (int8) and V (fp16) within
 // ~32 MB of the 126 MB L2, balanced in size (24-48 MB measured best on C2 and C4;
-// scripts/l2sweep.sh).
+// scripts/rounds/r01/l2sweep.sh).
 int raster_group_units(const AttnParams& p, int d) {
     static const size_t budget = [] {  // SAB_L2_GROUP_MB overrides the default (tuning)
         const char* e = std::getenv("SAB_L2_GROUP_MB");
