@@ -97,8 +97,9 @@ typedef struct sab_ws_layout {
     uint64_t mean_k;    /* float [units][head_dim]          SmoothState::mean_k        */
     uint64_t partials;  /* float [units][n_partials][head_dim] mean tree partial sums  */
     uint64_t v16;       /* fp16  [units][tokens][head_dim]  V on the fp16 grid (F32 in)*/
-    uint64_t status;    /* int32 device status word, followed by one int32 counter
-                           per unit (K1's mean tree; zero between calls)             */
+    uint64_t status;    /* int32 device status word, two int32 K2 scheduler counters,
+                           then one int32 counter per unit (K1's mean tree); all zero
+                           between calls                                              */
     uint64_t total;     /* workspace bytes                                            */
     int32_t n_partials; /* subtree sums per unit of the pairwise mean tree            */
     int32_t tree_depth; /* depth of the 4..9-token leaf level (quant.hpp:203-213)     */

@@ -165,13 +165,25 @@ struct Cfg {
     static constexpr int kOffBiasA = kOffV + kStages * kVBytes;
     static constexpr int kOffBiasB = kOffBiasA + 8192;
     static constexpr int kOffBar = kOffBiasB + 4096;
-    static constexpr int kSmemBytes = kOffBar + 512 + 1024;  // barriers + alignment slack
+    static constexpr int kSmemBytes = kOffBar + 1024 + 1024;  // barriers + alignment slack
 };
 
-struct Bars {  // must fit the 512 bytes reserved at Cfg::kOffBar
+// One K2 work item: a unit's query-tile pair (qt0, qt0 + 1), or a KV chunk of it.
+struct Item {
+    int it;  // index in the launch's item order (>= p.items: no more work)
+    int unit, pair, chunk, qt0, nkv_a, nkv_b, nkv, j0, nch;
+    int has_b;
+};
+
+struct Bars {  // must fit the 1024 bytes reserved at Cfg::kOffBar
     uint64_t q_full;
     uint64_t kv_full[16], kv_empty[16];
     uint64_t s_full[2][3], p_full[2][3], pv_done[2][3], o_final[2];
+    // Persistent work loop: the producer publishes each work item in a 2-slot ring;
+    // q_free: the item's last QK^T MMA has read Q^ (its buffer may be refilled);
+    // o_free[x]: the item's epilogue has read O_x (the next item's first PV may overwrite it).
+    uint64_t item_full[2], item_empty[2], q_free, o_free[2];
+    Item items[2];  // the decoded items of the ring (consumers read them in place)
     uint32_t tmem_base;
     int split_last;  // KV split: this CTA finished its pair's last chunk and merges
 };
@@ -599,7 +611,7 @@ __device__ __forceinline__ void store_o32(const AttnParams& p, int unit, int qi,
 // (the online-softmax identity of attention.hpp:429-443 across chunks).  Partials are
 // stored column-group-major ([item][d/4][256 rows] float4) so a warp's accesses coalesce.
 template <int D, bool OUT_F32>
-__device__ __noinline__ void split_epilogue(const AttnParams& p, Bars* bars, uint32_t t_o, int unit, int pair,
+__device__ __forceinline__ void split_epilogue(const AttnParams& p, Bars* bars, uint32_t t_o, int unit, int pair,
                                             int npair, int chunk, int nch, int x, int row, int half, int qi,
                                             bool valid, float m, float l) {
     const size_t pair_idx = static_cast<size_t>(unit) * npair + pair;
@@ -657,38 +669,35 @@ __device__ __noinline__ void split_epilogue(const AttnParams& p, Bars* bars, uin
     bool finite = true;
 #pragma unroll 1
     for (int c = 0; c < D / 2; c += 32) {
-        uint32_t own[32];
-        if (valid) {
-            tmem_ld16x2_32o<D / 2>(t_o + c, own);
-            tmem_wait_ld();
-        }
         float v[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = 0.0f;
         const int g0 = (half * (D / 2) + c) / 4;
 #pragma unroll 1
         for (int s = 0; s < nch; ++s) {
+            if (s == chunk && !valid) continue;  // (warp-uniform) this tile has no O in this chunk
             const float2 ml = s == chunk ? make_float2(m, l) : __ldcg(&p.part_ml[(item0 + s) * 256 + r]);
-            if (ml.x == -INFINITY) continue;  // no key of chunk s is visible to the row
-            const float w = ex2(ml.x - mm);
-            float4 t[8];
+            // A row with no visible key in chunk s contributes nothing; the TMEM load of the own
+            // chunk is warp-collective, so that case weighs its (zero) O by 0 instead of skipping.
+            if (s != chunk && ml.x == -INFINITY) continue;
+            const float w = ml.x == -INFINITY ? 0.0f : ex2(ml.x - mm);
+            uint32_t t[32];  // chunk s's 32 columns: this CTA's own O from TMEM, a peer's from L2
             if (s == chunk) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    t[e] = make_float4(__uint_as_float(own[4 * e]), __uint_as_float(own[4 * e + 1]),
-                                       __uint_as_float(own[4 * e + 2]), __uint_as_float(own[4 * e + 3]));
+                tmem_ld16x2_32o<D / 2>(t_o + c, t);
+                tmem_wait_ld();
             } else {
                 const float4* src = reinterpret_cast<const float4*>(p.part_o) + (item0 + s) * (D / 4) * 256 + r;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) t[e] = __ldcg(src + (g0 + e) * 256);
+                for (int e = 0; e < 8; ++e) {
+                    const float4 q4 = __ldcg(src + (g0 + e) * 256);
+                    t[4 * e] = __float_as_uint(q4.x);
+                    t[4 * e + 1] = __float_as_uint(q4.y);
+                    t[4 * e + 2] = __float_as_uint(q4.z);
+                    t[4 * e + 3] = __float_as_uint(q4.w);
+                }
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                v[4 * e] = fmaf(w, t[e].x, v[4 * e]);
-                v[4 * e + 1] = fmaf(w, t[e].y, v[4 * e + 1]);
-                v[4 * e + 2] = fmaf(w, t[e].z, v[4 * e + 2]);
-                v[4 * e + 3] = fmaf(w, t[e].w, v[4 * e + 3]);
-            }
+            for (int e = 0; e < 32; ++e) v[e] = fmaf(w, __uint_as_float(t[e]), v[e]);
         }
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
@@ -700,14 +709,303 @@ __device__ __noinline__ void split_epilogue(const AttnParams& p, Bars* bars, uin
     if (qi < p.n && !finite) atomicOr(p.status, kStatusOverflow);
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
+// Item `it` of the launch's linear item order (the order the hardware block scheduler
+// would dispatch the non-persistent grid in).
+template <bool CAUSAL, bool DUMP>
+__device__ __forceinline__ Item decode_item(const AttnParams& p, int it, int ntq, int ntk, int npair) {
+    Item w;
+    w.it = it;
+    w.chunk = 0;
+    if (DUMP) {
+        w.unit = p.dump_unit;
+        w.pair = p.dump_qtile / 2;
+    } else if (p.kv_chunk > 0) {
+        // KV split: items are enumerated chunk-major, longest pairs first inside a chunk.
+        // Pair work (KV tiles) is nondecreasing in the pair index, so chunk c exists for
+        // pairs [split_pmin(c), npair) -- no empty items, no item table.
+        int idx = it;
+        for (;; ++w.chunk) {
+            const int cnt = (npair - split_pmin(w.chunk * p.kv_chunk, npair, ntq, ntk, CAUSAL)) * p.units;
+            if (idx < cnt) break;
+            idx -= cnt;
+        }
+        w.unit = idx % p.units;
+        w.pair = npair - 1 - idx / p.units;
+    } else {
+        // Raster: units are taken in groups whose K^/V fit in L2 together (group_units,
+        // chosen by the host), so each K^/V tile is fetched from HBM about once and
+        // re-read from L2 by every query-tile pair of its unit.  Inside a group the
+        // longest pairs go first (causal work grows with the pair index).
+        const int gu = p.group_units;
+        const int g = it / (gu * npair);
+        const int r = it - g * gu * npair;
+        const int gsz = min(gu, p.units - g * gu);
+        w.unit = g * gu + r % gsz;
+        w.pair = npair - 1 - r / gsz;
+    }
+    w.qt0 = 2 * w.pair;
+    w.has_b = w.qt0 + 1 < ntq;
+    // Causal: query tile qt (rows < 128(qt+1)) needs KV tiles j with 64j <= 128qt + 127.
+    w.nkv_a = CAUSAL ? min(2 * w.qt0 + 2, ntk) : ntk;
+    w.nkv_b = w.has_b ? (CAUSAL ? min(2 * w.qt0 + 4, ntk) : ntk) : 0;
+    // KV split: this item covers the pair's KV tiles [j0, j0 + kv_chunk); pairs with a
+    // single chunk run the unsplit epilogue.  Kernel loops count j from j0 (ring stages,
+    // barrier phases); kb / TMA coordinates use j0 + j.
+    w.j0 = 0;
+    w.nch = 1;
+    if (!DUMP && p.kv_chunk > 0) {
+        const int nkv_full = max(w.nkv_a, w.nkv_b);
+        w.nch = (nkv_full + p.kv_chunk - 1) / p.kv_chunk;
+        w.j0 = w.chunk * p.kv_chunk;
+        const int j1 = min(nkv_full, w.j0 + p.kv_chunk);
+        w.nkv_a = max(0, min(w.nkv_a, j1) - w.j0);
+        w.nkv_b = max(0, min(w.nkv_b, j1) - w.j0);
+    }
+    w.nkv = max(w.nkv_a, w.nkv_b);
+    return w;
+}
+
+// Consumer side of the item ring: waits for item number n_it of this CTA and returns its
+// decoded form in shared memory.  Consumers read its fields in place (volatile: at the point
+// of use, so they do not hold registers across the softmax loop) until release_item.
+__device__ __forceinline__ const volatile Item* take_item(Bars* bars, int n_it) {
+    const int slot = n_it & 1;
+    mbar_wait(smem_u32(&bars->item_full[slot]), (n_it >> 1) & 1);
+    return &bars->items[slot];
+}
+
+// The warp is done with item n_it (one arrival per warp): its slot may be refilled.
+__device__ __forceinline__ void release_item(Bars* bars, int n_it, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&bars->item_empty[n_it & 1]));
+}
+
+// Phase parity of S buffer b's (j / NB)-th use in the current item: `ph` holds, per
+// buffer, the parity of its uses by earlier items (S tiles index buffers item-locally,
+// j % NB, so the unrolled loop keeps compile-time buffer addresses).
+__device__ __forceinline__ uint32_t buf_parity(uint32_t ph, int b, int use) { return ((ph >> b) ^ use) & 1u; }
+
+// Advances the per-buffer parities past an item of n S tiles.
+template <int NB>
+__device__ __forceinline__ uint32_t advance_parity(uint32_t ph, int n) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) ph ^= (static_cast<uint32_t>((n + NB - 1 - b) / NB) & 1u) << b;
+    return ph;
+}
+
+// One work item of a softmax warp (tile x = warp / 8): the online softmax over the item's
+// KV tiles, then the epilogue (or the KV-split epilogue).  ph: S-buffer parities (see
+// buf_parity); co: earlier items with work for tile x (o_final / o_free phases).
+// SPLIT: the item is one chunk of a KV-split pair (split_epilogue).
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8, bool SPLIT>
+__device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, uint32_t tbase, int warp, int lane,
+                                             const volatile Item* wi, uint32_t ph, int co) {
+    using C = Cfg<D>;
+    constexpr int NB = C::kNB;
+    const int n = p.n;
+    const int ntq = (n + kBM - 1) / kBM;
+    const int ntk = (n + kBN - 1) / kBN;
+    const int npair = (ntq + 1) / 2;
+    const int x = warp / 8;
+    const int lane_base = (warp % 4) * 32 + ((warp % 8) / 4) * 16;
+    const int half = lane / 16;
+    const int row = lane_base + (lane % 16);
+    const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
+    const uint32_t t_o = tbase + lane_off + C::kOffO + x * D;
+    // The item's fields, once into (warp-uniform) registers.
+    const int it_unit = __shfl_sync(0xffffffffu, wi->unit, 0);
+    const int it_j0 = __shfl_sync(0xffffffffu, wi->j0, 0);
+    const int it_qt = __shfl_sync(0xffffffffu, wi->qt0, 0) + x;
+#define SAB_UNIT it_unit
+#define SAB_J0 it_j0
+#define SAB_QT it_qt
+#define SAB_QI (it_qt * kBM + row)
+    const int nkv_x = __shfl_sync(0xffffffffu, x == 0 ? wi->nkv_a : wi->nkv_b, 0);
+    float m = -INFINITY, l = 0.0f;
+    if (nkv_x > 0) {
+        // Scale rows: per block [units][ntq] / [units][ntk]; per token (T) [units][npad],
+        // npad = ntk * 64 (K1 pads each unit's rows so 64-key tiles stay in bounds).
+        const int npad = ntk * kBN;
+        const float qsl = PT ? (SAB_QI < n ? p.qscales[static_cast<size_t>(SAB_UNIT) * npad + SAB_QI] : 1.0f) * kLog2e
+                             : p.qscales[static_cast<size_t>(SAB_UNIT) * ntq + SAB_QT] * kLog2e;
+        const float* ksc = p.kscales + static_cast<size_t>(SAB_UNIT) * (PT ? npad : ntk);
+        // The K scale of the next KV tile is fetched one iteration ahead.
+        float ks_next = PT ? 0.0f : __ldg(ksc + SAB_J0);
+        const bool tr = (warp % 8) == 0 && lane == 0;
+        // Software pipeline: S(j+1) is loaded from TMEM while P(j) is stored and
+        // handed to the MMA issuer, so the load latency is off the per-tile chain.
+        uint32_t r[32];
+        if (tr) SAB_STAMP(x, 0, 0);
+        mbar_wait(smem_u32(&bars->s_full[x][0]), buf_parity(ph, 0, 0));
+        tc_fence_after();
+        tmem_ld16x2_32(tbase + lane_off + x * (NB * 64), r);
+#pragma unroll(PT ? 1 : 2)  // B: compile-time buffer parity per copy (+1-2 %); T would spill
+        for (int j = 0; j < nkv_x; ++j) {
+            const float ks_cur = ks_next;
+            if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + SAB_J0 + j + 1);
+            const int b = j % NB;
+            tmem_wait_ld_dep(r);
+            if (tr) SAB_STAMP(x, j, 1);
+            const uint32_t t_s = tbase + lane_off + x * (NB * 64) + b * 64;
+            int32_t* dump = (DUMP && SAB_QT == p.dump_qtile)
+                                ? p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN + 32 * half
+                                : nullptr;
+            const int kb = (SAB_J0 + j) * kBN;
+            // Dequant factor of this 64-key group: dQ * dK * log2(e), so that p = 2^(s - m).
+            const float cg = qsl * ks_cur;
+            const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > SAB_QT * kBM);
+            bool rescale;
+            float alpha;
+            if (VI8 && PT) {
+                const float* dkp = ksc + kb + 32 * half;
+                if (p.diag)  // static-scale diagnostics (rare, slow path)
+                    alpha = need_mask ? softmax_half_pt_i8<true, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, SAB_QI, n,
+                                                                               m, l, rescale, p.diag, SAB_J0 + j == 0)
+                                      : softmax_half_pt_i8<false, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, SAB_QI,
+                                                                                n, m, l, rescale, p.diag,
+                                                                                SAB_J0 + j == 0);
+                else if (need_mask)
+                    alpha = softmax_half_pt_i8<true, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, SAB_QI, n, m, l,
+                                                                    rescale, nullptr, false);
+                else
+                    alpha = softmax_half_pt_i8<false, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, SAB_QI, n, m, l,
+                                                                     rescale, nullptr, false);
+            } else if (VI8) {
+                if (p.diag)
+                    alpha = need_mask ? softmax_half_i8<true, CAUSAL, true>(r, t_s, half, cg, kb, SAB_QI, n, m, l,
+                                                                            rescale, p.diag, SAB_J0 + j == 0)
+                                      : softmax_half_i8<false, CAUSAL, true>(r, t_s, half, cg, kb, SAB_QI, n, m, l,
+                                                                             rescale, p.diag, SAB_J0 + j == 0);
+                else if (need_mask)
+                    alpha = softmax_half_i8<true, CAUSAL, false>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
+                                                                 nullptr, false);
+                else
+                    alpha = softmax_half_i8<false, CAUSAL, false>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
+                                                                  nullptr, false);
+            } else if (PT) {
+                const float* dkp = ksc + kb + 32 * half;
+                if (need_mask)
+                    alpha = softmax_half_pt<true, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, SAB_QI, n,
+                                                                           m, l, rescale, dump, j == 0);
+                else
+                    alpha = softmax_half_pt<false, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, SAB_QI, n,
+                                                                            m, l, rescale, dump, j == 0);
+            } else if (need_mask) {
+                alpha = softmax_half<true, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
+                                                                    dump, tr ? x : -1, j);
+            } else {
+                alpha = softmax_half<false, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
+                                                                     dump, tr ? x : -1, j);
+            }
+            if (tr) SAB_STAMP(x, j, 2);
+            if (rescale && j > 0) {
+                // O_x must hold P(j-1)V(j-1) before it is rescaled: PV_x(j-1) has finished
+                // accumulating (per-buffer barriers keep the phase unambiguous; PV_x(j-1+NB)
+                // needs P from a later step).  Thread halves split O's columns.
+                const int pj = j - 1;
+                mbar_wait(smem_u32(&bars->pv_done[x][pj % NB]), buf_parity(ph, pj % NB, pj / NB));
+                tc_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < D / 2; c += 32) {
+                    uint32_t o[32];
+                    tmem_ld16x2_32o<D / 2>(t_o + c, o);
+                    tmem_wait_ld();
+                    if (VI8) {
+                        // INT32 O: O <- rne(alpha * O).  The rounding (<= 0.5 of a code product
+                        // per move of the row max) is far below P~'s own 1/254 step.
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            o[e] = static_cast<uint32_t>(
+                                __float2int_rn(static_cast<float>(static_cast<int>(o[e])) * alpha));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                    }
+                    tmem_st16x2_32o<D / 2>(t_o + c, o);
+                }
+            }
+            tmem_wait_st();  // P (and rescaled O) are in TMEM
+            if (tr) SAB_STAMP(x, j, 3);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));  // one arrival per warp
+            if (tr) SAB_STAMP(x, j, 4);
+            if (j + 1 < nkv_x) {  // S(j+1) is issued into TMEM registers now; waited at the loop top
+                if (tr) SAB_STAMP(x, j + 1, 0);
+                const int nj = j + 1;
+                mbar_wait(smem_u32(&bars->s_full[x][nj % NB]), buf_parity(ph, nj % NB, nj / NB));
+                tc_fence_after();
+                tmem_ld16x2_32(tbase + lane_off + x * (NB * 64) + (nj % NB) * 64, r);
+            }
+        }
+
+        // -------------------------------------------------------- epilogue
+        mbar_wait(smem_u32(&bars->o_final[x]), co & 1);
+        tc_fence_after();
+        if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 3);
+        l += __shfl_xor_sync(0xffffffffu, l, 16);  // the two column halves of the row
+        if (!DUMP && !SPLIT) {  // (KV-split chunks: split_epilogue below)
+            const float inv_l = 1.0f / l;
+            bool finite = true;
+#pragma unroll 1
+            for (int c = 0; c < D / 2; c += 32) {
+                uint32_t o[32];
+                tmem_ld16x2_32o<D / 2>(t_o + c, o);
+                tmem_wait_ld();
+                float v[32];
+                if (VI8) {
+                    // (float(acc) * dP) * dV[c] (attention.hpp:494-495), then 1/l (536-538).
+                    const float4* vs4 = reinterpret_cast<const float4*>(
+                        p.vscales + static_cast<size_t>(SAB_UNIT) * D + half * (D / 2) + c);
+#pragma unroll
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const float4 vs = __ldg(vs4 + e4);
+                        const float wv[4] = {vs.x, vs.y, vs.z, vs.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int e = 4 * e4 + i;
+                            v[e] = ((static_cast<float>(static_cast<int>(o[e])) * (1.0f / 127.0f)) * wv[i]) *
+                                   inv_l;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        finite &= isfinite(__uint_as_float(o[e]));
+                        v[e] = __uint_as_float(o[e]) * inv_l;
+                    }
+                }
+                if (SAB_QI < n) store_o32<D, OUT_F32>(p, SAB_UNIT, SAB_QI, half * (D / 2) + c, v);
+            }
+            if (SAB_QI < n && !finite) atomicOr(p.status, kStatusOverflow);
+        }
+        if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 4);
+    }
+    if constexpr (!DUMP && !VI8 && SPLIT)
+        split_epilogue<D, OUT_F32>(p, bars, t_o, SAB_UNIT, wi->pair, npair, wi->chunk, wi->nch, x, row, half, SAB_QI,
+                                   nkv_x > 0, m, l);
+    if (nkv_x > 0) {  // O_x has been read: the next item's first PV may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars->o_free[x]));
+    }
+#undef SAB_UNIT
+#undef SAB_J0
+#undef SAB_QT
+#undef SAB_QI
+}
+
+
+// KSPLIT: the launch has a KV-split plan (kv_chunk > 0).  A separate instantiation: the
+// split epilogue's code in the item loop would cost the common kernel its registers.
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8, bool KSPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     k2_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
     using C = Cfg<D>;
     constexpr int S = C::kStages;
     constexpr int NB = C::kNB;
-    static_assert(sizeof(Bars) <= 512, "barrier block overflows its reservation");
+    static_assert(sizeof(Bars) <= 1024, "barrier block overflows its reservation");
     static_assert(C::kOffO + 2 * D <= 512, "TMEM budget");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -726,53 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ntk = (n + kBN - 1) / kBN;
     const int npair = (ntq + 1) / 2;
 
-    int unit, pair, chunk = 0;
-    if (DUMP) {
-        unit = p.dump_unit;
-        pair = p.dump_qtile / 2;
-    } else if (p.kv_chunk > 0) {
-        // KV split: items are enumerated chunk-major, longest pairs first inside a chunk.
-        // Pair work (KV tiles) is nondecreasing in the pair index, so chunk c exists for
-        // pairs [split_pmin(c), npair) -- no empty CTAs, no item table.
-        int idx = static_cast<int>(blockIdx.x);
-        for (;; ++chunk) {
-            const int cnt = (npair - split_pmin(chunk * p.kv_chunk, npair, ntq, ntk, CAUSAL)) * p.units;
-            if (idx < cnt) break;
-            idx -= cnt;
-        }
-        unit = idx % p.units;
-        pair = npair - 1 - idx / p.units;
-    } else {
-        // Raster: units are taken in groups whose K^/V fit in L2 together (group_units,
-        // chosen by the host), so each K^/V tile is fetched from HBM about once and
-        // re-read from L2 by every query-tile pair of its unit.  Inside a group the
-        // longest pairs go first (causal work grows with the pair index).
-        const int gu = p.group_units;
-        const int g = static_cast<int>(blockIdx.x) / (gu * npair);
-        const int r = static_cast<int>(blockIdx.x) - g * gu * npair;
-        const int gsz = min(gu, p.units - g * gu);
-        unit = g * gu + r % gsz;
-        pair = npair - 1 - r / gsz;
-    }
-    const int qt0 = 2 * pair;
-    const bool has_b = qt0 + 1 < ntq;
-    // Causal: query tile qt (rows < 128(qt+1)) needs KV tiles j with 64j <= 128qt + 127.
-    int nkv_a = CAUSAL ? min(2 * qt0 + 2, ntk) : ntk;
-    int nkv_b = has_b ? (CAUSAL ? min(2 * qt0 + 4, ntk) : ntk) : 0;
-    // KV split (p.kv_chunk > 0, grid.y = chunk): this CTA covers the pair's KV tiles
-    // [j0, j0 + kv_chunk); pairs with a single chunk run the unsplit epilogue.  Below,
-    // j counts tiles from j0 (ring stages, barrier phases); kb / TMA coordinates use j0 + j.
-    int j0 = 0, nch = 1;
-    if (!DUMP && p.kv_chunk > 0) {
-        const int nkv_full = max(nkv_a, nkv_b);
-        nch = (nkv_full + p.kv_chunk - 1) / p.kv_chunk;
-        j0 = chunk * p.kv_chunk;
-        const int j1 = min(nkv_full, j0 + p.kv_chunk);
-        nkv_a = max(0, min(nkv_a, j1) - j0);
-        nkv_b = max(0, min(nkv_b, j1) - j0);
-    }
-    const int nkv = max(nkv_a, nkv_b);
-
+    if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 0);  // CTA lifecycle (SAB_TRACE builds)
     {  // constant operands of the bias MMA, written once through the generic proxy
         uint4* bias = reinterpret_cast<uint4*>(smem + C::kOffBiasA);
         const uint4 a2048 = make_uint4(0x68006800u, 0x68006800u, 0x68006800u, 0x68006800u);
@@ -793,7 +1045,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_init(smem_u32(&bars->pv_done[x][b]), 1);
             }
             mbar_init(smem_u32(&bars->o_final[x]), 1);
+            mbar_init(smem_u32(&bars->o_free[x]), 8);  // one arrival per softmax warp of tile x
         }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&bars->item_full[i]), 1);
+            mbar_init(smem_u32(&bars->item_empty[i]), 17);  // MMA warp + 16 softmax warps
+        }
+        mbar_init(smem_u32(&bars->q_free), 1);
         fence_barrier_init();
     }
     if (warp == 16) tmem_alloc<512>(smem_u32(&bars->tmem_base));
@@ -801,41 +1059,82 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = bars->tmem_base;
+    if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 1);
     // Everything above is independent of K1; Q^/K^/scales/V are read only below.
     griddep_wait();
+    if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 2);
 
+    // Work loop.  Every role walks the same sequence of items; barrier phases run on
+    // state that continues across items (K^/V ring tiles g, S-buffer parities ph[x], items
+    // with work for tile x co[x]), so an item's prologue (Q^ and K^/V loads, the first QK^T
+    // MMAs) overlaps the previous item's epilogue.  Non-persistent launches (p.persist 0:
+    // one CTA per item) run the loop once.
+    const int n_items = DUMP ? 1 : p.items;
     if (warp == 16) {
-        // ------------------------------------------------------------ TMA producer
+        // ------------------------------------------------------------ TMA producer + scheduler
         if (lane == 0) {
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
-            mbar_arrive_expect_tx(smem_u32(&bars->q_full), (has_b ? 2 : 1) * C::kQBytes);
-            tma_load_3d(sQ, &tm_q, smem_u32(&bars->q_full), 0, qt0 * kBM, unit);
-            if (has_b) tma_load_3d(sQ + C::kQBytes, &tm_q, smem_u32(&bars->q_full), 0, (qt0 + 1) * kBM, unit);
-            for (int j = 0; j < nkv; ++j) {
-                const int s = j % S;
-                const uint32_t ph = (j / S) & 1;
-                SAB_STAMP(4, j, 0);
-                mbar_wait(smem_u32(&bars->kv_empty[s]), ph ^ 1);
-                SAB_STAMP(4, j, 1);
-                const uint32_t full = smem_u32(&bars->kv_full[s]);
+        }
+        int it = DUMP ? 0 : static_cast<int>(blockIdx.x);
+        uint32_t g = 0;
+        for (int n_it = 0;; ++n_it) {
+            const int slot = n_it & 1;
+            const Item w = decode_item<CAUSAL, DUMP>(p, it < n_items ? it : 0, ntq, ntk, npair);
+            if (lane == 0) {
+                if (n_it >= 2) mbar_wait(smem_u32(&bars->item_empty[slot]), ((n_it - 2) >> 1) & 1);
+                bars->items[slot] = w;
+                bars->items[slot].it = it;
+                mbar_arrive(smem_u32(&bars->item_full[slot]));
+            }
+            __syncwarp();
+            if (it >= n_items) break;
+            if (lane == 0) {
+                if (n_it >= 1) mbar_wait(smem_u32(&bars->q_free), (n_it - 1) & 1);
+                mbar_arrive_expect_tx(smem_u32(&bars->q_full), (w.has_b ? 2 : 1) * C::kQBytes);
+                tma_load_3d(sQ, &tm_q, smem_u32(&bars->q_full), 0, w.qt0 * kBM, w.unit);
+                if (w.has_b)
+                    tma_load_3d(sQ + C::kQBytes, &tm_q, smem_u32(&bars->q_full), 0, (w.qt0 + 1) * kBM, w.unit);
+                for (int j = 0; j < w.nkv; ++j, ++g) {
+                    const int s = g % S;
+                    const uint32_t ph = (g / S) & 1;
+                    SAB_STAMP(4, j, 0);
+                    mbar_wait(smem_u32(&bars->kv_empty[s]), ph ^ 1);
+                    SAB_STAMP(4, j, 1);
+                    const uint32_t full = smem_u32(&bars->kv_full[s]);
 #ifdef SAB_SK_NOKV  // timing skeleton: K^/V loaded for the first ring fill only (wrong results)
-                if (j >= S) {
-                    mbar_arrive(full);
-                    continue;
-                }
+                    if (g >= S) {
+                        mbar_arrive(full);
+                        continue;
+                    }
 #endif
-                mbar_arrive_expect_tx(full, C::kKBytes + (VI8 ? kBN * D : C::kVBytes));
-                const int key0 = (j0 + j) * kBN;
-                tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, key0, unit);
-                if (VI8) {  // V^ transposed: D channel rows of 64 key codes (K-major B operand)
-                    tma_load_3d(sV + s * C::kVBytes, &tm_v, full, key0, 0, unit);
-                } else {
+                    mbar_arrive_expect_tx(full, C::kKBytes + (VI8 ? kBN * D : C::kVBytes));
+                    const int key0 = (w.j0 + j) * kBN;
+                    tma_load_3d(sK + s * C::kKBytes, &tm_k, full, 0, key0, w.unit);
+                    if (VI8) {  // V^ transposed: D channel rows of 64 key codes (K-major B operand)
+                        tma_load_3d(sV + s * C::kVBytes, &tm_v, full, key0, 0, w.unit);
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < D / 64; ++c)
-                        tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, key0, unit);
+                        for (int c = 0; c < D / 64; ++c)
+                            tma_load_3d(sV + s * C::kVBytes + c * C::kVChunk, &tm_v, full, c * 64, key0, w.unit);
+                    }
                 }
+                // Next item: dynamic (an atomic counter after the first, static item per CTA)
+                // when persistent; the loop ends after one item otherwise.
+                it = (!DUMP && p.persist) ? atomicAdd(p.sched, 1) + static_cast<int>(gridDim.x) : n_items;
+            } else {
+                g += w.nkv;
+            }
+            it = __shfl_sync(0xffffffffu, it, 0);
+        }
+        if (!DUMP && p.persist && lane == 0) {
+            // The last CTA out resets the scheduler for the next launch on this workspace.
+            __threadfence();
+            if (atomicAdd(p.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+                p.sched[0] = 0;
+                p.sched[1] = 0;
+                __threadfence();
             }
         }
         __syncwarp();
@@ -855,81 +1154,114 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t idesc_bias = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 0, kBM, kBN);
         const uint64_t d_bias_a = make_smem_desc(smem_u32(smem + C::kOffBiasA), 128, 256, kSwizzleNone);
         const uint64_t d_bias_b = make_smem_desc(smem_u32(smem + C::kOffBiasB), 128, 256, kSwizzleNone);
-        if (nkv > 0) mbar_wait(smem_u32(&bars->q_full), 0);
-        // QK_x(j) into S_x[j%2].  Issued after PV_x(j-2), which read P_x(j-2) from that
-        // buffer (tcgen05 ops of one thread execute in issue order).
-        auto issue_qk = [&](int x, int j) {
-            const int s = j % S;
-            const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
-            const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
-            const uint32_t t_s = tbase + x * (NB * 64) + (j % NB) * 64;
-            if (elect_one()) {
-                // Bias MMA: S = 2^23 + 2^22 as binary32 (bits 0x4B400000) from constant fp16
-                // operands, then the INT32 QK^T products accumulate onto those bits, so the
-                // softmax reads float(2^23 + 2^22 + acc) directly.
+        uint32_t g = 0;
+        uint32_t ph[2] = {0u, 0u};
+        int co[2] = {0, 0};
+        for (int n_it = 0;; ++n_it) {
+            const volatile Item* wi = take_item(bars, n_it);
+            // Broadcast through a shuffle so the compiler knows the loop state is warp-uniform
+            // (uniform registers: no per-MMA R2UR sequences).
+            if (__shfl_sync(0xffffffffu, wi->it, 0) >= n_items) break;
+            const int nkv_a = __shfl_sync(0xffffffffu, wi->nkv_a, 0);
+            const int nkv_b = __shfl_sync(0xffffffffu, wi->nkv_b, 0);
+            const int nkv = max(nkv_a, nkv_b);
+            mbar_wait(smem_u32(&bars->q_full), n_it & 1);
+            // QK_x(j) into S_x[j % NB].  Issued after PV_x(j-2), which read P_x(j-2)
+            // from that buffer (tcgen05 ops of one thread execute in issue order).
+            auto issue_qk = [&](int x, int j) {
+                const int s = (g + j) % S;
+                const uint64_t dq = dq0 + static_cast<uint64_t>((x * C::kQBytes) >> 4);
+                const uint64_t dk = dk0 + static_cast<uint64_t>((s * C::kKBytes) >> 4);
+                const int sb = j % NB;
+                const uint32_t t_s = tbase + x * (NB * 64) + sb * 64;
+                if (elect_one()) {
+                    // Bias MMA: S = 2^23 + 2^22 as binary32 (bits 0x4B400000) from constant fp16
+                    // operands, then the INT32 QK^T products accumulate onto those bits, so the
+                    // softmax reads float(2^23 + 2^22 + acc) directly.
 #ifndef SAB_SK_NOBIAS  // timing skeleton: no bias MMA (wrong results)
-                umma_f16_ss(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
+                    umma_f16_ss(t_s, d_bias_a, d_bias_b, idesc_bias, 0u);
 #endif
 #pragma unroll
-                for (int kk = 0; kk < D / 32; ++kk)
-                    umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2), idesc_qk,
+                    for (int kk = 0; kk < D / 32; ++kk)
+                        umma_i8_ss(t_s, dq + static_cast<uint64_t>(kk * 2), dk + static_cast<uint64_t>(kk * 2),
+                                   idesc_qk,
 #ifdef SAB_SK_NOBIAS
-                               kk > 0 ? 1u : 0u);
+                                   kk > 0 ? 1u : 0u);
 #else
-                               1u);
+                                   1u);
 #endif
-                umma_commit(smem_u32(&bars->s_full[x][j % NB]));
+                    umma_commit(smem_u32(&bars->s_full[x][sb]));
+                }
+                __syncwarp();
+            };
+            auto wait_kv = [&](int j) {
+                if (lane == 0) SAB_STAMP(2, j, 0);
+                mbar_wait(smem_u32(&bars->kv_full[(g + j) % S]), ((g + j) / S) & 1);
+                tc_fence_after();
+                if (lane == 0) SAB_STAMP(2, j, 1);
+            };
+            // Q^ is free for the next item once the item's last QK^T MMA has completed.
+            auto release_q = [&]() {
+                if (elect_one()) umma_commit(smem_u32(&bars->q_free));
+                __syncwarp();
+            };
+            for (int j = 0; j < NB && j < nkv; ++j) {
+                wait_kv(j);
+                if (j < nkv_a) issue_qk(0, j);
+                if (j < nkv_b) issue_qk(1, j);
             }
-            __syncwarp();
-        };
-        auto wait_kv = [&](int j) {
-            if (lane == 0) SAB_STAMP(2, j, 0);
-            mbar_wait(smem_u32(&bars->kv_full[j % S]), (j / S) & 1);
-            tc_fence_after();
-            if (lane == 0) SAB_STAMP(2, j, 1);
-        };
-        for (int j = 0; j < NB && j < nkv; ++j) {
-            wait_kv(j);
-            if (j < nkv_a) issue_qk(0, j);
-            if (j < nkv_b) issue_qk(1, j);
-        }
-        for (int j = 0; j < nkv; ++j) {
-            const int s = j % S;
-            const bool next = j + NB < nkv;
-            if (next) wait_kv(j + NB);
+            if (nkv <= NB) release_q();
+            for (int j = 0; j < nkv; ++j) {
+                const int s = (g + j) % S;
+                const bool next = j + NB < nkv;
+                if (next) wait_kv(j + NB);
 #pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    const int nkv_x = x == 0 ? nkv_a : nkv_b;
+                    if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
+                        const int sb = j % NB;
+                        if (j == 0 && co[x] > 0) {  // the previous item's epilogue has read O_x
+                            mbar_wait(smem_u32(&bars->o_free[x]), (co[x] - 1) & 1);
+                            tc_fence_after();
+                        }
+                        if (lane == 0) SAB_STAMP(2 + x, j, 3);
+                        mbar_wait(smem_u32(&bars->p_full[x][sb]), buf_parity(ph[x], sb, j / NB));
+                        tc_fence_after();
+                        if (lane == 0) SAB_STAMP(2 + x, j, 4);
+                        const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
+                        const uint32_t t_p = tbase + x * (NB * 64) + sb * 64;
+                        const uint32_t t_o = tbase + C::kOffO + x * D;
+                        if (elect_one()) {
+                            if (VI8) {  // INT32 O_x += P~^(j) V^(j): 2 x K=32 codes, P~^ from TMEM
+#pragma unroll
+                                for (int kk = 0; kk < kBN / 32; ++kk)
+                                    umma_i8_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * 2), idesc_pv8,
+                                               (j > 0 || kk > 0) ? 1u : 0u);
+                            } else {
+#pragma unroll
+                                for (int kk = 0; kk < kBN / 16; ++kk)
+                                    umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)),
+                                                idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+                            }
+                            umma_commit(smem_u32(&bars->pv_done[x][sb]));
+                            if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
+                        }
+                        __syncwarp();
+                        if (lane == 0) SAB_STAMP(2 + x, j, 5);
+                    }
+                    if (next && j + NB < nkv_x) issue_qk(x, j + NB);
+                }
+                if (next && j + NB == nkv - 1) release_q();
+                if (elect_one()) umma_commit(smem_u32(&bars->kv_empty[s]));  // K^(j), V(j) free once these MMAs finish
+                __syncwarp();
+            }
+            release_item(bars, n_it, lane);
+            g += nkv;
             for (int x = 0; x < 2; ++x) {
                 const int nkv_x = x == 0 ? nkv_a : nkv_b;
-                if (j < nkv_x) {  // O_x += P_x(j) V(j), P from TMEM
-                    if (lane == 0) SAB_STAMP(2 + x, j, 3);
-                    mbar_wait(smem_u32(&bars->p_full[x][j % NB]), (j / NB) & 1);
-                    tc_fence_after();
-                    if (lane == 0) SAB_STAMP(2 + x, j, 4);
-                    const uint64_t dv = dv0 + static_cast<uint64_t>((s * C::kVBytes) >> 4);
-                    const uint32_t t_p = tbase + x * (NB * 64) + (j % NB) * 64;
-                    const uint32_t t_o = tbase + C::kOffO + x * D;
-                    if (elect_one()) {
-                        if (VI8) {  // INT32 O_x += P~^(j) V^(j): 2 x K=32 codes, P~^ from TMEM
-#pragma unroll
-                            for (int kk = 0; kk < kBN / 32; ++kk)
-                                umma_i8_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * 2), idesc_pv8,
-                                           (j > 0 || kk > 0) ? 1u : 0u);
-                        } else {
-#pragma unroll
-                            for (int kk = 0; kk < kBN / 16; ++kk)
-                                umma_f16_ts(t_o, t_p + kk * 8, dv + static_cast<uint64_t>(kk * (2048 >> 4)),
-                                            idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-                        }
-                        umma_commit(smem_u32(&bars->pv_done[x][j % NB]));
-                        if (j == nkv_x - 1) umma_commit(smem_u32(&bars->o_final[x]));
-                    }
-                    __syncwarp();
-                    if (lane == 0) SAB_STAMP(2 + x, j, 5);
-                }
-                if (next && j + NB < nkv_x) issue_qk(x, j + NB);
+                ph[x] = advance_parity<NB>(ph[x], nkv_x);
+                co[x] += nkv_x > 0;
             }
-            if (elect_one()) umma_commit(smem_u32(&bars->kv_empty[s]));  // K^(j), V(j) free once these MMAs finish
-            __syncwarp();
         }
         __syncwarp();
     } else if (warp < 16) {
@@ -937,177 +1269,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Tile x = warp / 8.  Warp w covers TMEM lanes [32(w%4) + 16((w%8)/4), +16); its
         // threads t and t+16 share one query row (t % 16) and split the columns.
         const int x = warp / 8;
-        const int qt = qt0 + x;
-        const int nkv_x = x == 0 ? nkv_a : nkv_b;
-        const int lane_base = (warp % 4) * 32 + ((warp % 8) / 4) * 16;
-        const int half = lane / 16;
-        const int row = lane_base + (lane % 16);
-        const uint32_t lane_off = static_cast<uint32_t>(lane_base) << 16;
-        const uint32_t t_o = tbase + lane_off + C::kOffO + x * D;
-        const int qi = qt * kBM + row;
-        float m = -INFINITY, l = 0.0f;
-        if (nkv_x > 0) {
-            // Scale rows: per block [units][ntq] / [units][ntk]; per token (T) [units][npad],
-            // npad = ntk * 64 (K1 pads each unit's rows so 64-key tiles stay in bounds).
-            const int npad = ntk * kBN;
-            const float qsl = PT ? (qi < n ? p.qscales[static_cast<size_t>(unit) * npad + qi] : 1.0f) * kLog2e
-                                 : p.qscales[static_cast<size_t>(unit) * ntq + qt] * kLog2e;
-            const float* ksc = p.kscales + static_cast<size_t>(unit) * (PT ? npad : ntk);
-            // The K scale of the next KV tile is fetched one iteration ahead.
-            float ks_next = PT ? 0.0f : __ldg(ksc + j0);
-            const bool tr = (warp % 8) == 0 && lane == 0;
-            // Software pipeline: S(j+1) is loaded from TMEM while P(j) is stored and
-            // handed to the MMA issuer, so the load latency is off the per-tile chain.
-            uint32_t r[32];
-            if (tr) SAB_STAMP(x, 0, 0);
-            mbar_wait(smem_u32(&bars->s_full[x][0]), 0);
-            tc_fence_after();
-            tmem_ld16x2_32(tbase + lane_off + x * (NB * 64), r);
-#pragma unroll(PT ? 1 : 2)  // B: compile-time buffer parity per copy (+1-2 %); T would spill
-            for (int j = 0; j < nkv_x; ++j) {
-                const float ks_cur = ks_next;
-                if (!PT && j + 1 < nkv_x) ks_next = __ldg(ksc + j0 + j + 1);
-                const int b = j % NB;
-                tmem_wait_ld_dep(r);
-                if (tr) SAB_STAMP(x, j, 1);
-                const uint32_t t_s = tbase + lane_off + x * (NB * 64) + b * 64;
-                int32_t* dump = (DUMP && qt == p.dump_qtile)
-                                    ? p.s_dump + (static_cast<size_t>(j) * kBM + row) * kBN + 32 * half
-                                    : nullptr;
-                const int kb = (j0 + j) * kBN;
-                // Dequant factor of this 64-key group: dQ * dK * log2(e), so that p = 2^(s - m).
-                const float cg = qsl * ks_cur;
-                const bool need_mask = (kb + kBN > n) || (CAUSAL && kb + kBN - 1 > qt * kBM);
-                bool rescale;
-                float alpha;
-                if (VI8 && PT) {
-                    const float* dkp = ksc + kb + 32 * half;
-                    if (p.diag)  // static-scale diagnostics (rare, slow path)
-                        alpha = need_mask ? softmax_half_pt_i8<true, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, qi, n, m,
-                                                                                   l, rescale, p.diag, j0 + j == 0)
-                                          : softmax_half_pt_i8<false, CAUSAL, true>(r, t_s, half, qsl, dkp, kb, qi, n,
-                                                                                    m, l, rescale, p.diag, j0 + j == 0);
-                    else if (need_mask)
-                        alpha = softmax_half_pt_i8<true, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale,
-                                                                        nullptr, false);
-                    else
-                        alpha = softmax_half_pt_i8<false, CAUSAL, false>(r, t_s, half, qsl, dkp, kb, qi, n, m, l,
-                                                                         rescale, nullptr, false);
-                } else if (VI8) {
-                    if (p.diag)
-                        alpha = need_mask ? softmax_half_i8<true, CAUSAL, true>(r, t_s, half, cg, kb, qi, n, m, l,
-                                                                                rescale, p.diag, j0 + j == 0)
-                                          : softmax_half_i8<false, CAUSAL, true>(r, t_s, half, cg, kb, qi, n, m, l,
-                                                                                 rescale, p.diag, j0 + j == 0);
-                    else if (need_mask)
-                        alpha = softmax_half_i8<true, CAUSAL, false>(r, t_s, half, cg, kb, qi, n, m, l, rescale,
-                                                                     nullptr, false);
-                    else
-                        alpha = softmax_half_i8<false, CAUSAL, false>(r, t_s, half, cg, kb, qi, n, m, l, rescale,
-                                                                      nullptr, false);
-                } else if (PT) {
-                    const float* dkp = ksc + kb + 32 * half;
-                    if (need_mask)
-                        alpha = softmax_half_pt<true, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale, dump,
-                                                                       j == 0);
-                    else
-                        alpha = softmax_half_pt<false, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, qi, n, m, l, rescale,
-                                                                        dump, j == 0);
-                } else if (need_mask) {
-                    alpha = softmax_half<true, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
-                } else {
-                    alpha = softmax_half<false, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, qi, n, m, l, rescale, dump, tr ? x : -1, j);
-                }
-                if (tr) SAB_STAMP(x, j, 2);
-                if (rescale && j > 0) {
-                    // O_x must hold P(j-1)V(j-1) before it is rescaled.  PV_x(j-2) is complete
-                    // (QK_x(j) was issued after it), so parity (j-1)&1 of pv_done is unambiguous.
-                    // Thread halves split O's columns.
-                    // PV_x(j-1) has finished accumulating into O_x (per-buffer barriers keep
-                    // the phase unambiguous; PV_x(j-1+NB) needs P from a later step).
-                    mbar_wait(smem_u32(&bars->pv_done[x][(j - 1) % NB]), ((j - 1) / NB) & 1);
-                    tc_fence_after();
-#pragma unroll 1
-                    for (int c = 0; c < D / 2; c += 32) {
-                        uint32_t o[32];
-                        tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                        tmem_wait_ld();
-                        if (VI8) {
-                            // INT32 O: O <- rne(alpha * O).  The rounding (<= 0.5 of a code product
-                            // per move of the row max) is far below P~'s own 1/254 step.
-#pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                o[e] = static_cast<uint32_t>(
-                                    __float2int_rn(static_cast<float>(static_cast<int>(o[e])) * alpha));
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                        }
-                        tmem_st16x2_32o<D / 2>(t_o + c, o);
-                    }
-                }
-                tmem_wait_st();  // P (and rescaled O) are in TMEM
-                if (tr) SAB_STAMP(x, j, 3);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bars->p_full[x][b]));  // one arrival per warp
-                if (tr) SAB_STAMP(x, j, 4);
-                if (j + 1 < nkv_x) {  // S(j+1) is issued into TMEM registers now; waited at the loop top
-                    if (tr) SAB_STAMP(x, j + 1, 0);
-                    mbar_wait(smem_u32(&bars->s_full[x][(j + 1) % NB]), ((j + 1) / NB) & 1);
-                    tc_fence_after();
-                    tmem_ld16x2_32(tbase + lane_off + x * (NB * 64) + ((j + 1) % NB) * 64, r);
-                }
-            }
-
-            // -------------------------------------------------------- epilogue
-            mbar_wait(smem_u32(&bars->o_final[x]), 0);
-            tc_fence_after();
-            l += __shfl_xor_sync(0xffffffffu, l, 16);  // the two column halves of the row
-            if (!DUMP && nch == 1) {  // (KV-split chunks: split_epilogue below)
-                const float inv_l = 1.0f / l;
-                bool finite = true;
-#pragma unroll 1
-                for (int c = 0; c < D / 2; c += 32) {
-                    uint32_t o[32];
-                    tmem_ld16x2_32o<D / 2>(t_o + c, o);
-                    tmem_wait_ld();
-                    float v[32];
-                    if (VI8) {
-                        // (float(acc) * dP) * dV[c] (attention.hpp:494-495), then 1/l (536-538).
-                        const float4* vs4 = reinterpret_cast<const float4*>(
-                            p.vscales + static_cast<size_t>(unit) * D + half * (D / 2) + c);
-#pragma unroll
-                        for (int e4 = 0; e4 < 8; ++e4) {
-                            const float4 vs = __ldg(vs4 + e4);
-                            const float w[4] = {vs.x, vs.y, vs.z, vs.w};
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const int e = 4 * e4 + i;
-                                v[e] = ((static_cast<float>(static_cast<int>(o[e])) * (1.0f / 127.0f)) * w[i]) * inv_l;
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            finite &= isfinite(__uint_as_float(o[e]));
-                            v[e] = __uint_as_float(o[e]) * inv_l;
-                        }
-                    }
-                    if (qi < n) store_o32<D, OUT_F32>(p, unit, qi, half * (D / 2) + c, v);
-                }
-                if (qi < n && !finite) atomicOr(p.status, kStatusOverflow);
-            }
+        uint32_t ph = 0u;
+        int co = 0;
+        for (int n_it = 0;; ++n_it) {
+            const volatile Item* wi = take_item(bars, n_it);
+            if (__shfl_sync(0xffffffffu, wi->it, 0) >= n_items) break;
+            const int nkv_x = __shfl_sync(0xffffffffu, x == 0 ? wi->nkv_a : wi->nkv_b, 0);
+            if (KSPLIT && wi->nch > 1)
+                softmax_item<D, CAUSAL, OUT_F32, false, PT, false, true>(p, bars, tbase, warp, lane, wi, ph, co);
+            else
+                softmax_item<D, CAUSAL, OUT_F32, DUMP, PT, VI8, false>(p, bars, tbase, warp, lane, wi, ph, co);
+            release_item(bars, n_it, lane);
+            ph = advance_parity<C::kNB>(ph, nkv_x);
+            co += nkv_x > 0;
         }
-        if (!DUMP && !VI8 && nch > 1)
-            split_epilogue<D, OUT_F32>(p, bars, t_o, unit, pair, npair, chunk, nch, x, row, half, qi, nkv_x > 0, m, l);
     }
 
+    if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 5);
     tc_fence_before();
     __syncthreads();
     if (warp == 16) {
         tc_fence_after();
         tmem_dealloc<512>(tbase);
+        if (lane == 0) SAB_STAMP(4, kTraceTiles - 1, 6);
     }
 }
 
@@ -1141,6 +1325,22 @@ bool make_map(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int ele
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// SMs of the current device (one persistent K2 CTA each).
+int sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+// SAB_K2_PERSIST: unset -> heuristic (launch_k2), 0 -> never, 1 -> always.
+int k2_persist_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("SAB_K2_PERSIST");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    return mode;
+}
+
 // Raster groups: as few groups as keep each group's K^ (int8) and V (fp16) within
 // ~32 MB of the 126 MB L2, balanced in size (24-48 MB measured best on C2 and C4;
 // scripts/rounds/r01/l2sweep.sh).
@@ -1156,8 +1356,8 @@ int raster_group_units(const AttnParams& p, int d) {
     return static_cast<int>((static_cast<size_t>(p.units) + groups - 1) / groups);
 }
 
-template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
-cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8, bool KSPLIT>
+cudaError_t launch_k2_split(const AttnParams& p, cudaStream_t s) {
     using C = Cfg<D>;
     CUtensorMap tq, tk, tv;
     const CUtensorMapSwizzle swqk = D == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
@@ -1170,23 +1370,39 @@ cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
         return cudaErrorInvalidValue;
     AttnParams pp = p;
     pp.group_units = raster_group_units(p, D);
-    auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP, PT, VI8>;
+    auto kern = k2_attention<D, CAUSAL, OUT_F32, DUMP, PT, VI8, KSPLIT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int ntq = (p.n + kBM - 1) / kBM;
     const int npair = (ntq + 1) / 2, ntk = (p.n + kBN - 1) / kBN;
-    unsigned grid = DUMP ? 1u : static_cast<unsigned>(npair) * static_cast<unsigned>(p.units);
-    if (!DUMP && p.kv_chunk > 0) {  // one CTA per (unit, pair, chunk) item
-        long long items = 0;
+    long long items = DUMP ? 1 : static_cast<long long>(npair) * p.units;
+    if (!DUMP && p.kv_chunk > 0) {  // one item per (unit, pair, chunk)
+        items = 0;
         for (int c = 0; c < p.nchunk; ++c)
             items += static_cast<long long>(npair - split_pmin(c * p.kv_chunk, npair, ntq, ntk, CAUSAL)) * p.units;
-        grid = static_cast<unsigned>(items);
     }
+    pp.items = static_cast<int>(items);
+    // Persistent (one CTA per SM walks the items, the next item's Q^/K^/V loads and first
+    // QK^T MMAs overlapping the current item's epilogue) where the per-item fixed cost
+    // matters: causal grids (uneven items, C2 +2.5 %) and short ones (<= 8 items per SM:
+    // C4 N=1K +11..19 %).  Long uniform grids (C3, C4 N>=4K non-causal) measured 1-2 %
+    // faster with one CTA per item.  SAB_K2_PERSIST=0 / 1 forces either.
+    const int sms = sm_count();
+    const int mode = k2_persist_mode();
+    pp.persist = !DUMP && items > sms && (mode == 1 || (mode < 0 && (CAUSAL || items <= 8LL * sms)));
+    const unsigned grid = static_cast<unsigned>(pp.persist ? sms : items);
 #ifdef SAB_TRACE
     cudaMemcpyToSymbolAsync(g_trace, &h_trace_ptr, sizeof(h_trace_ptr), 0, cudaMemcpyHostToDevice, s);
     cudaMemcpyToSymbolAsync(g_trace_cta, &h_trace_cta, sizeof(int), 0, cudaMemcpyHostToDevice, s);
 #endif
     return launch_pdl(kern, dim3(grid), dim3(kThreads), C::kSmemBytes, s, tq, tk, tv, pp);
+}
+
+template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8>
+cudaError_t launch_k2(const AttnParams& p, cudaStream_t s) {
+    if constexpr (!DUMP && !VI8)  // the INT8 P~V path and the INT32 dump never split
+        if (p.kv_chunk > 0) return launch_k2_split<D, CAUSAL, OUT_F32, DUMP, PT, VI8, true>(p, s);
+    return launch_k2_split<D, CAUSAL, OUT_F32, DUMP, PT, VI8, false>(p, s);
 }
 
 template <bool DUMP, bool PT, bool VI8 = false>

@@ -69,7 +69,7 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     const size_t items = kv_chunk ? units * npair * size_t(nchunk) : 0;
     // Everything a call must find zeroed is contiguous (one memset per call, see
     // reset_bytes): status word + per-unit K1 counters, static-scale counters, split counters.
-    L->status = take(sizeof(int32_t) * (1 + units));
+    L->status = take(sizeof(int32_t) * (3 + units));  // word, K2 scheduler [2], K1 per-unit counters
     L->diag = take(2 * sizeof(unsigned long long));
     L->split_cnt = take(kv_chunk ? 2 * units * npair * sizeof(int32_t) : 0);
     L->vcodes = take(pv8 ? units * hd * npad : 0);
@@ -110,7 +110,7 @@ PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const vo
         p.ldv = (d->tokens + kBlockKV - 1) / kBlockKV * kBlockKV;
     }
     p.status = at<int>(ws, L.status);
-    p.counters = p.status + 1;
+    p.counters = p.status + 3;
     p.units = int(units_of(d));
     p.n = d->tokens;
     p.d = d->head_dim;
@@ -142,6 +142,7 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
     }
     a.o = o;
     a.status = at<int>(w, L.status);
+    a.sched = a.status + 1;
     a.units = int(units_of(d));
     a.n = d->tokens;
     a.d = d->head_dim;

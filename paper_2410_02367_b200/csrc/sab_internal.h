@@ -81,6 +81,11 @@ struct AttnParams {
     // KV split (sab_ws_layout::kv_chunk): chunk c of a pair covers KV tiles
     // [c * kv_chunk, (c + 1) * kv_chunk); grid.y = nchunk.
     int kv_chunk, nchunk;
+    // Persistent K2 (set by launch_attention): `items` work items over min(items, SMs)
+    // CTAs, taken from the self-resetting counters sched[0] (next item) / sched[1] (CTAs
+    // done) in the status block; persist == 0: one CTA per item.
+    int items, persist;
+    int* sched;
     float* part_o;          // [units][npair][nchunk][d/4][256] float4 groups of unnormalised partial O
     float2* part_ml;        // [units][npair][nchunk][256] (m, l)
     int* split_cnt;         // [units][npair][2] chunks finished / partials written (self-resetting)

@@ -1,6 +1,6 @@
 """Runs one K2 launch with the SAB_TRACE build and dumps one CTA's clock64 timeline.
 
-    python scripts/trace_k2.py <workload> <cta> <out.npy>     (libsageattn_b200.so must be a SAB_TRACE build)
+    python scripts/trace_k2.py <workload> <cta> <out.npy> [units]   (libsageattn_b200.so must be a SAB_TRACE build)
 """
 import ctypes as C
 import os
@@ -16,6 +16,8 @@ from paper_2410_02367_b200 import _lib, sageattn  # noqa: E402
 wl = bench.workload(sys.argv[1])
 cta = int(sys.argv[2])
 b, h, n, d, causal = wl["batch"], wl["heads"], wl["tokens"], wl["head_dim"], wl["causal"]
+if len(sys.argv) > 4:  # optional unit count (a K3 shard), as (1, units)
+    b, h = 1, int(sys.argv[4])
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(0)
 q, k, v = (torch.randn((b, h, n, d), generator=g, device=dev).half() for _ in range(3))
