@@ -290,7 +290,7 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
             pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
         }
         pk[i] = pack_half2(pp.x, pp.y);
-        acc[i & 3] = fadd2(acc[i & 3], pp);
+        acc[i & 3] = i < 4 ? pp : fadd2(acc[i & 3], pp);  // (the first four start the chains)
     }
     if (trole >= 0) SAB_STAMP(trole, ttile, 7);
     tmem_st16x2_16(ts, pk);
@@ -427,7 +427,7 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
                     pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
                 }
                 pk[c / 2] = pack_half2(pp.x, pp.y);
-                acc[g & 3] = fadd2(acc[g & 3], pp);
+                acc[g & 3] = (g < 4 && e == 0) ? pp : fadd2(acc[g & 3], pp);
                 pm[g & 3] = fmaxf(pm[g & 3], fmaxf(pp.x, pp.y));
             }
         }
@@ -490,7 +490,7 @@ __device__ __forceinline__ float softmax_half_pt(uint32_t (&r)[32], uint32_t ts,
             pp.y = (c + 1 >= lim2) ? 0.0f : pp.y;
         }
         pk[i] = pack_half2(pp.x, pp.y);
-        acc[i & 3] = fadd2(acc[i & 3], pp);
+        acc[i & 3] = i < 4 ? pp : fadd2(acc[i & 3], pp);
     }
     tmem_st16x2_16(ts, pk);
     const f2 sum = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
