@@ -474,6 +474,13 @@ def main():
     lay = _lib.SabWsLayout()
     _lib.check(_lib.load().sab_workspace_layout(ctypes.byref(desc), ctypes.byref(lay)))
     config["kv_split"] = {"kv_chunk_tiles": lay.kv_chunk, "chunks": lay.kv_nchunk} if lay.kv_chunk else "off"
+    # K2's launch mode, mirroring launch_k2's heuristic (persistent for causal or <= 8 items/SM).
+    sms_dev = torch.cuda.get_device_properties(dev).multi_processor_count
+    k2_items = count * ((-(-n // 128) + 1) // 2) if not lay.kv_chunk else None
+    persist_env = os.environ.get("SAB_K2_PERSIST")
+    many = k2_items is None or k2_items > sms_dev
+    config["k2_launch"] = ("persistent" if many and (persist_env == "1" or (persist_env is None and (
+        causal or (k2_items is not None and k2_items <= 8 * sms_dev)))) else "one CTA per item")
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream

@@ -944,7 +944,31 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
         tc_fence_after();
         if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 3);
         l += __shfl_xor_sync(0xffffffffu, l, 16);  // the two column halves of the row
-        if (!DUMP && !SPLIT) {  // (KV-split chunks: split_epilogue below)
+        if (!DUMP && !SPLIT && !VI8) {
+            // Both column blocks of O come out of TMEM behind one wait; O_x is then released to
+            // the next item's first PV (persistent launches) before the normalise-and-store.
+            const float inv_l = 1.0f / l;
+            bool finite = true;
+            uint32_t o[D / 2];
+#pragma unroll
+            for (int c = 0; c < D / 2; c += 32)
+                tmem_ld16x2_32o<D / 2>(t_o + c, *reinterpret_cast<uint32_t(*)[32]>(o + c));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars->o_free[x]));
+#pragma unroll
+            for (int c = 0; c < D / 2; c += 32) {
+                float v[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    finite &= isfinite(__uint_as_float(o[c + e]));
+                    v[e] = __uint_as_float(o[c + e]) * inv_l;
+                }
+                if (SAB_QI < n) store_o32<D, OUT_F32>(p, SAB_UNIT, SAB_QI, half * (D / 2) + c, v);
+            }
+            if (SAB_QI < n && !finite) atomicOr(p.status, kStatusOverflow);
+        } else if (!DUMP && !SPLIT) {  // VI8 (KV-split chunks: split_epilogue below)
             const float inv_l = 1.0f / l;
             bool finite = true;
 #pragma unroll 1
@@ -984,7 +1008,7 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
     if constexpr (!DUMP && !VI8 && SPLIT)
         split_epilogue<D, OUT_F32>(p, bars, t_o, SAB_UNIT, wi->pair, npair, wi->chunk, wi->nch, x, row, half, SAB_QI,
                                    nkv_x > 0, m, l);
-    if (nkv_x > 0) {  // O_x has been read: the next item's first PV may overwrite it
+    if (nkv_x > 0 && (DUMP || SPLIT || VI8)) {  // O_x has been read: the next item's first PV may overwrite it
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bars->o_free[x]));
