@@ -584,9 +584,37 @@ __host__ __device__ __forceinline__ int split_pmin(int t0, int npair, int ntq, i
 }
 
 // One softmax thread's 32 output values of row qi, columns [col, col + 32), to O.
+__device__ __forceinline__ void st_global_v8(void* dst, const uint32_t (&w)[8]) {  // one 32-byte store
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+
 template <int D, bool OUT_F32>
 __device__ __forceinline__ void store_o32(const AttnParams& p, int unit, int qi, int col, const float (&v)[32]) {
     const size_t off = (static_cast<size_t>(unit) * p.n + qi) * D + col;
+    if (p.o_v8) {  // 32-byte stores (O 32-byte aligned): half the store instructions, whole sectors
+        if (OUT_F32) {
+            float* dst = static_cast<float*>(p.o) + off;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                uint32_t w[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = __float_as_uint(v[8 * e + i]);
+                st_global_v8(dst + 8 * e, w);
+            }
+        } else {
+            __half* dst = static_cast<__half*>(p.o) + off;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                uint32_t w[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = pack_half2(v[16 * e + 2 * i], v[16 * e + 2 * i + 1]);
+                st_global_v8(dst + 16 * e, w);
+            }
+        }
+        return;
+    }
     if (OUT_F32) {
         float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.o) + off);
 #pragma unroll
@@ -799,7 +827,7 @@ __device__ __forceinline__ uint32_t advance_parity(uint32_t ph, int n) {
 // SPLIT: the item is one chunk of a KV-split pair (split_epilogue).
 template <int D, bool CAUSAL, bool OUT_F32, bool DUMP, bool PT, bool VI8, bool SPLIT>
 __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, uint32_t tbase, int warp, int lane,
-                                             const volatile Item* wi, uint32_t ph, int co) {
+                                             const volatile Item* wi, uint32_t ph, int co, int n_it) {
     using C = Cfg<D>;
     constexpr int NB = C::kNB;
     const int n = p.n;
@@ -836,6 +864,7 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
         // handed to the MMA issuer, so the load latency is off the per-tile chain.
         uint32_t r[32];
         if (tr) SAB_STAMP(x, 0, 0);
+        if (threadIdx.x == 0) SAB_STAMP(4, 400 + n_it, 1);  // per-item timeline (SAB_TRACE builds)
         mbar_wait(smem_u32(&bars->s_full[x][0]), buf_parity(ph, 0, 0));
         tc_fence_after();
         tmem_ld16x2_32(tbase + lane_off + x * (NB * 64), r);
@@ -943,6 +972,7 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
         mbar_wait(smem_u32(&bars->o_final[x]), co & 1);
         tc_fence_after();
         if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 3);
+        if (threadIdx.x == 0) SAB_STAMP(4, 400 + n_it, 3);
         l += __shfl_xor_sync(0xffffffffu, l, 16);  // the two column halves of the row
         if (!DUMP && !SPLIT && !VI8) {
             // Both column blocks of O come out of TMEM behind one wait; O_x is then released to
@@ -1004,6 +1034,7 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
             if (SAB_QI < n && !finite) atomicOr(p.status, kStatusOverflow);
         }
         if (threadIdx.x == 0) SAB_STAMP(4, kTraceTiles - 1, 4);
+        if (threadIdx.x == 0) SAB_STAMP(4, 400 + n_it, 4);
     }
     if constexpr (!DUMP && !VI8 && SPLIT)
         split_epilogue<D, OUT_F32>(p, bars, t_o, SAB_UNIT, wi->pair, npair, wi->chunk, wi->nch, x, row, half, SAB_QI,
@@ -1299,10 +1330,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const volatile Item* wi = take_item(bars, n_it);
             if (__shfl_sync(0xffffffffu, wi->it, 0) >= n_items) break;
             const int nkv_x = __shfl_sync(0xffffffffu, x == 0 ? wi->nkv_a : wi->nkv_b, 0);
+            if (threadIdx.x == 0) SAB_STAMP(4, 400 + n_it, 0);
             if (KSPLIT && wi->nch > 1)
-                softmax_item<D, CAUSAL, OUT_F32, false, PT, false, true>(p, bars, tbase, warp, lane, wi, ph, co);
+                softmax_item<D, CAUSAL, OUT_F32, false, PT, false, true>(p, bars, tbase, warp, lane, wi, ph, co, n_it);
             else
-                softmax_item<D, CAUSAL, OUT_F32, DUMP, PT, VI8, false>(p, bars, tbase, warp, lane, wi, ph, co);
+                softmax_item<D, CAUSAL, OUT_F32, DUMP, PT, VI8, false>(p, bars, tbase, warp, lane, wi, ph, co, n_it);
+            if (threadIdx.x == 0) SAB_STAMP(4, 400 + n_it, 5);
             release_item(bars, n_it, lane);
             ph = advance_parity<C::kNB>(ph, nkv_x);
             co += nkv_x > 0;

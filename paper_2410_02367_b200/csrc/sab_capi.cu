@@ -141,6 +141,7 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
         a.ldv = (d->tokens + kBlockKV - 1) / kBlockKV * kBlockKV;
     }
     a.o = o;
+    a.o_v8 = (reinterpret_cast<uintptr_t>(o) & 31u) == 0;
     a.status = at<int>(w, L.status);
     a.sched = a.status + 1;
     a.units = int(units_of(d));

@@ -85,6 +85,7 @@ struct AttnParams {
     // CTAs, taken from the self-resetting counters sched[0] (next item) / sched[1] (CTAs
     // done) in the status block; persist == 0: one CTA per item.
     int items, persist;
+    int o_v8;  // O is 32-byte aligned: the epilogue writes with 32-byte stores
     int* sched;
     float* part_o;          // [units][npair][nchunk][d/4][256] float4 groups of unnormalised partial O
     float2* part_ml;        // [units][npair][nchunk][256] (m, l)

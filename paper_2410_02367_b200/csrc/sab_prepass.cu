@@ -30,6 +30,7 @@
 // __float2int_rn reproduce the reference's binary32 operations one for one.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "sab_internal.h"
@@ -310,6 +311,7 @@ __device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, i
 
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
+    griddep_launch_dependents();  // k1_quantize's input loads may start behind this grid
     mean_partial<T, D, G>(p, blockIdx.y, blockIdx.x);
 }
 
@@ -440,7 +442,10 @@ __global__ void __launch_bounds__(kQThreads) k1_quantize(PrepassParams p) {
         bulk_load(smem_u32(sq), static_cast<const T*>(p.q) + ubase + static_cast<size_t>(r0) * D, bytes, smem_u32(&bar));
         bulk_load(smem_u32(sk), static_cast<const T*>(p.k) + ubase + static_cast<size_t>(r0) * D, bytes, smem_u32(&bar));
     }
-    // mean_k (computed by k1_mean_partials; zero when smoothing is off).
+    // mean_k (computed by k1_mean_partials; zero when smoothing is off).  The chunk's Q and K
+    // loads (inputs) are in flight before the wait for the producer grid (PDL launch).
+    griddep_wait();
+    griddep_launch_dependents();  // K2 may be scheduled behind this grid's last wave
     if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
     __syncthreads();
     mbar_wait(smem_u32(&bar), 0);
@@ -984,10 +989,23 @@ cudaError_t launch_v(const PrepassParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// The fp16 per-block path for few-unit calls (K3 shards: C2 on 8 GPUs = 4 units) runs as
+// k1_mean_partials -> k1_quantize (Q and K of a chunk together, both loads in flight before
+// the PDL wait for mean(K)) instead of (mean partials + Q chunks) -> (K chunks): with few
+// units the first kernel's Q chunks are the long pole (C2 8-GPU shard K1 28.5 -> 25 us);
+// with many units it is 5-15 % slower.  SAB_K1_ALT=0 / 1 forces either.
+bool k1_alt(const PrepassParams& p) {
+    static const int mode = [] {
+        const char* e = std::getenv("SAB_K1_ALT");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    return mode >= 0 ? mode == 1 : p.units <= 8;
+}
+
 template <typename T, int D>
 cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
-    if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope) {
+    if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && !k1_alt(p)) {
         const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
         constexpr int smem = kBlockQ * D * 2;
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
@@ -1020,6 +1038,7 @@ cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int smem = 2 * kBlockQ * D * static_cast<int>(sizeof(T));
     cudaError_t e = cudaFuncSetAttribute(k1_quantize<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    if (p.smooth) return launch_pdl(k1_quantize<T, D>, grid, dim3(kQThreads), smem, s, p);
     k1_quantize<T, D><<<grid, kQThreads, smem, s>>>(p);
     return cudaGetLastError();
 }

@@ -27,3 +27,25 @@ def test_persistent_equals_one_cta_per_item(cuda, tmp_path):
     for key in a.files:
         assert np.isfinite(a[key]).all(), key
         assert np.array_equal(a[key].view(np.uint32), b[key].view(np.uint32)), key
+
+
+@pytest.mark.parametrize("out_f32", [False, True])
+def test_output_alignment_paths_agree(cuda, out_f32):
+    """O written with 32-byte stores (32-byte aligned O) and with 16-byte stores (O only 16-byte
+    aligned, the C ABI's minimum) is bit-identical."""
+    import torch
+
+    from paper_2410_02367_b200 import sage_attention_cuda
+
+    shape = (1, 3, 700, 128)
+    g = torch.Generator(device=cuda).manual_seed(7)
+    q, k, v = (torch.randn(shape, generator=g, device=cuda).half() for _ in range(3))
+    dt = torch.float32 if out_f32 else torch.float16
+    a = sage_attention_cuda(q, k, v, causal=True, out_dtype=dt)
+    n = a.numel()
+    shift = 16 // a.element_size()  # 16 bytes: aligned for the ABI, not for 32-byte stores
+    buf = torch.empty(n + shift, dtype=dt, device=cuda)
+    b = buf[shift:].view(shape)
+    assert b.data_ptr() % 32 == 16
+    sage_attention_cuda(q, k, v, causal=True, out=b, out_dtype=dt)
+    assert torch.equal(a, b)
