@@ -941,11 +941,25 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
                     tmem_wait_ld();
                     if (VI8) {
                         // INT32 O: O <- rne(alpha * O).  The rounding (<= 0.5 of a code product
-                        // per move of the row max) is far below P~'s own 1/254 step.
+                        // per move of the row max) is far below P~'s own 1/254 step.  Done on the
+                        // FMA/ALU pipes: y + (2^23 + 2^22) leaves rne(y) in the low mantissa bits
+                        // for |y| < 2^22 (alpha <= 1 keeps |y| <= |O|); a chunk holding a larger
+                        // value takes the cvt.rni path (XU pipe, shared with the exponentials).
+                        float y[32];
+                        float ymax = 0.0f;
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            o[e] = static_cast<uint32_t>(
-                                __float2int_rn(static_cast<float>(static_cast<int>(o[e])) * alpha));
+                        for (int e = 0; e < 32; ++e) {
+                            y[e] = static_cast<float>(static_cast<int>(o[e])) * alpha;
+                            ymax = fmaxf(ymax, fabsf(y[e]));
+                        }
+                        if (ymax < 4194304.0f) {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                o[e] = __float_as_uint(y[e] + kMagicF) - kMagicI;
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] = static_cast<uint32_t>(__float2int_rn(y[e]));
+                        }
                     } else {
 #pragma unroll
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
