@@ -373,6 +373,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--pv-accum", default="fp32", choices=["fp32", "fp16"],
+                    help="B/T P~V accumulator: fp32 (default, the parity-gated arm) or the binary16 arm")
     ap.add_argument("--variant", default="B", choices=["B", "T", "VB", "VT"],
                     help="B: SAGEAttn-B (per-block Q/K scales, the north-star path); T: SAGEAttn-T (per-token)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -408,6 +410,8 @@ def main():
               "scaling_mode": args.scaling + (" (batch grows with GPUs; units per GPU fixed)" if args.scaling == "weak"
                                               else " (fixed workload sharded)"),
               "l2": "inputs (3 x fp16 Q/K/V) larger than L2, and L2 flushed between timed steps"}
+    if args.pv_accum != "fp32" and not pv_int8:
+        config["pv_accum"] = args.pv_accum
 
     if args.impl == "reference":
         if rank != 0:
@@ -469,7 +473,8 @@ def main():
     data = ("synthetic N(0,1) fp16 from the seeded counter RNG (global index; synth.tensor_torch, generated on "
             "the device), Q/K/V seeds 1/2/3")
     o = torch.empty_like(q)
-    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8)
+    desc = sageattn.make_desc(q, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8,
+                               pv_accum="fp32" if pv_int8 else args.pv_accum)
     ws = sageattn.Workspace(desc, dev)
     lay = _lib.SabWsLayout()
     _lib.check(_lib.load().sab_workspace_layout(ctypes.byref(desc), ctypes.byref(lay)))
@@ -509,7 +514,8 @@ def main():
         for gi, gc in enumerate(groups):
             sl = slice(g0, g0 + gc)
             gq, gk, gv, go = (t[:, sl] for t in (q, k, v, o))
-            gdesc = sageattn.make_desc(gq, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8)
+            gdesc = sageattn.make_desc(gq, causal, out_dtype=torch.float16, per_token=per_token, pv_int8=pv_int8,
+                                       pv_accum="fp32" if pv_int8 else args.pv_accum)
             gsteps.append((gdesc, sageattn.Workspace(gdesc, dev), gq, gk, gv, go,
                            stream if gi == 0 else torch.cuda.Stream(dev), torch.cuda.Event()))
             g0 += gc
@@ -567,14 +573,15 @@ def main():
     host = [t.reshape(1, count, n, d).cpu() for t in (q, k, v)]
     hq, hk, hv = (h.contiguous().pin_memory().numpy() for h in host)
     ho = torch.empty(hq.shape, dtype=torch.float16).pin_memory().numpy()
+    acc = "fp32" if pv_int8 else args.pv_accum
     sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token,
-                                pv_int8=pv_int8)  # warm pool
+                                pv_int8=pv_int8, pv_accum=acc)  # warm pool
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         sageattn.attention_fwd_host(hq, hk, hv, causal, ho, devices=[dev.index], per_token=per_token,
-                                    pv_int8=pv_int8)
+                                    pv_int8=pv_int8, pv_accum=acc)
     e2e_s = time.perf_counter() - t0
 
     local = torch.tensor([sum(t_step), sum(t_k1), sum(t_k2), e2e_s, sum(t_serial)], dtype=torch.float64,

@@ -28,8 +28,10 @@
 //     throw std::invalid_argument -- there is no CPU fallback for sage_attention;
 //   * head_dim must be 64 or 128;
 //   * P~V accumulates in FP32 on the tensor cores (the reference's
-//     pv_fp32_accumulator arm) whatever pv_fp32_accumulator says; Q^/K^ codes,
-//     scales and mean(K) are bit-identical to the reference.
+//     pv_fp32_accumulator arm) whatever pv_fp32_accumulator says, unless
+//     b200::honour_pv_accumulator_option() (SAB_PV_ACCUM=options) maps
+//     pv_fp32_accumulator == false to the binary16 TMEM accumulator; Q^/K^
+//     codes, scales and mean(K) are bit-identical to the reference.
 // naive_attention (the binary64 exact oracle, attention.hpp:107-149) and
 // flash_attention_fp (the binary32 tiled baseline, 169-252) are not on the
 // SageAttn path; they stay host functions here so programs that compare
@@ -40,6 +42,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <limits>
 #include <stdexcept>
 #include <string>
@@ -129,6 +132,19 @@ inline int& device_count_override() {
     return n;
 }
 
+// P~V accumulator of a drop-in call (B/T).  false (default): FP32 in TMEM whatever
+// SageOptions::pv_fp32_accumulator says -- the arm the parity gate is stated against.
+// true: honour the option as the reference does (attention.hpp:75, 447-475), so the
+// default pv_fp32_accumulator == false selects the binary16 TMEM accumulator
+// (SAB_PV_FP16).  Environment: SAB_PV_ACCUM=options sets it at first use.
+inline bool& honour_pv_accumulator_option() {
+    static bool on = [] {
+        const char* e = std::getenv("SAB_PV_ACCUM");
+        return e && std::string(e) == "options";
+    }();
+    return on;
+}
+
 // The sm_100 ordinals a call uses (never a device of another architecture).
 inline std::vector<int> devices_for_call() {
     int n = 0;
@@ -173,6 +189,10 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
     d.check_v = 1;  // validate_input scans V too (attention.hpp:101)
     d.qk_granularity = config.qk_granularity == QkGranularity::PerToken ? SAB_QK_PER_TOKEN : SAB_QK_PER_BLOCK;
     d.pv_path = config.pv_path == PvPath::Int8 ? SAB_PV_PATH_INT8 : SAB_PV_PATH_FP16;
+    d.pv_accum = (b200::honour_pv_accumulator_option() && d.pv_path == SAB_PV_PATH_FP16 &&
+                  !options.pv_fp32_accumulator)
+                     ? SAB_PV_FP16
+                     : SAB_PV_FP32;
     // attention.hpp:479: the static-scale counters exist only on the INT8 P~V path.
     SageDiagnostics* diag = options.diagnostics;
     d.measure_static_scale = (diag && diag->measure_static_scale && d.pv_path == SAB_PV_PATH_INT8) ? 1 : 0;

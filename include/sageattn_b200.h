@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SAB_ABI_VERSION 6
+#define SAB_ABI_VERSION 7
 
 /* Status codes.  The C++ shim maps them back to the reference's exceptions:
  * SAB_ERR_SHAPE / SAB_ERR_NONFINITE / SAB_ERR_UNSUPPORTED -> std::invalid_argument,
@@ -48,12 +48,18 @@ enum sab_status {
 
 enum sab_dtype { SAB_F16 = 0, SAB_F32 = 1 };
 
-/* PV accumulation: FP32 accumulator in TMEM, the arm of
- * SageOptions::pv_fp32_accumulator (attention.hpp:75, 454-471) -- the only one.
- * The reference's default persistent-binary16 accumulator drifts by 4e-3..1.6e-2
- * rel-L1 from its own FP32 arm, so no tensor-core accumulation order can
- * reproduce it within the 2e-3 gate; any other value is rejected. */
-enum sab_pv_accum { SAB_PV_FP32 = 0 };
+/* P~V accumulation (FP16 P~V path, variants B/T):
+ *   SAB_PV_FP32 -- FP32 accumulator in TMEM: the arm of SageOptions::pv_fp32_accumulator
+ *                  (attention.hpp:75, 454-471).  The default; the parity gate.
+ *   SAB_PV_FP16 -- one persistent binary16 accumulator per row in TMEM (tcgen05.mma
+ *                  kind::f16 with an F16 D, the paper's mma f16.f16.f16), rescaled with a
+ *                  binary16 rounding: the semantics of the reference's default arm
+ *                  (attention.hpp:447-475, matmul.hpp:63-73).  The tensor core rounds once
+ *                  per 16 products instead of after every addition, so it lands as far from
+ *                  that arm as the arm is from its own FP32 arm (4e-3..1.6e-2 rel-L1, SURVEY
+ *                  F3) and about 4x closer to the FP32 arm; a non-finite accumulator raises
+ *                  SAB_ERR_OVERFLOW as in the reference.  Never KV-split.  ABI 7. */
+enum sab_pv_accum { SAB_PV_FP32 = 0, SAB_PV_FP16 = 1 };
 
 /* Q/K scale granularity: KernelConfig::qk_granularity (attention.hpp:34, 41-46).
  * PER_BLOCK = SAGEAttn-B (128-token Q groups, 64-token K groups); PER_TOKEN =

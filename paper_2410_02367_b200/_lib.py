@@ -24,6 +24,7 @@ SAB_ERR_ARGUMENT = 8
 SAB_F16 = 0
 SAB_F32 = 1
 SAB_PV_FP32 = 0
+SAB_PV_FP16 = 1  # binary16 P~V accumulator (the paper's mma f16.f16.f16)
 SAB_QK_PER_BLOCK = 0  # SAGEAttn-B
 SAB_QK_PER_TOKEN = 1  # SAGEAttn-T
 SAB_PV_PATH_FP16 = 0  # B / T

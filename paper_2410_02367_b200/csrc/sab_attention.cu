@@ -136,6 +136,15 @@ __device__ __forceinline__ f2 exp2_poly2(f2 x) {
               __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23))};
 }
 
+// Binary16 P~V accumulator (AttnParams::pv16): a kind::f16 MMA with c_format F16 keeps one
+// value per 32-bit TMEM column, in the low half (upper half zero; scripts/micro/f16acc.cu).
+__device__ __forceinline__ float f16acc_get(uint32_t cell) {
+    return __half2float(__ushort_as_half(static_cast<unsigned short>(cell & 0xFFFFu)));
+}
+__device__ __forceinline__ uint32_t f16acc_put(float x) {
+    return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(x)));
+}
+
 template <int D>
 struct Cfg {
 #ifndef SAB_STAGES128
@@ -960,6 +969,11 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
 #pragma unroll
                             for (int e = 0; e < 32; ++e) o[e] = static_cast<uint32_t>(__float2int_rn(y[e]));
                         }
+                    } else if (p.pv16) {
+                        // Binary16 O: O <- rn16(alpha * O), the reference's snap of the rescaled
+                        // accumulator (attention.hpp:450-453).
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = f16acc_put(f16acc_get(o[e]) * alpha);
                     } else {
 #pragma unroll
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
@@ -1001,6 +1015,10 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bars->o_free[x]));
+            if (p.pv16) {  // binary16 accumulator cells -> fp32 (an infinite cell is the overflow)
+#pragma unroll
+                for (int e = 0; e < D / 2; ++e) o[e] = __float_as_uint(f16acc_get(o[e]));
+            }
 #pragma unroll
             for (int c = 0; c < D / 2; c += 32) {
                 float v[32];
@@ -1213,7 +1231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // tile j: PV_A(j), QK_A(j+2), PV_B(j), QK_B(j+2) -- one K^/V wait per tile for both
         // query tiles, and the two tiles' softmax phases interleave on the tensor pipe.
         constexpr uint32_t idesc_qk = make_idesc(2 /*S32*/, 1 /*S8*/, 1 /*S8*/, 0, 0, kBM, kBN);
-        constexpr uint32_t idesc_pv = make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
+        // P~V accumulator: F32 (SAB_PV_FP32), or F16 (SAB_PV_FP16, the paper's mma f16.f16.f16).
+        const uint32_t idesc_pv = p.pv16 ? make_idesc(0 /*F16*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D)
+                                         : make_idesc(1 /*F32*/, 0 /*F16*/, 0 /*F16*/, 0, 1 /*V MN-major*/, kBM, D);
         // Descriptors are advanced by adding (byte offset >> 4) to the start-address field.
         const uint64_t dq0 = make_smem_desc(sQ, 16, C::kSboQK, C::kSwizzleQK);
         const uint64_t dk0 = make_smem_desc(sK, 16, C::kSboQK, C::kSwizzleQK);

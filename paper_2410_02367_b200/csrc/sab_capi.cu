@@ -63,8 +63,9 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     L->v16 = take(d->in_dtype == SAB_F32 && !pv8 ? units * n * hd * 2 : 0);
     int kv_chunk = 0, nchunk = 1;
     // The INT8 P~V path quantizes P~ against the running row max (quantize_p_static,
-    // quant.hpp:258-279), so chunked maxima would change its codes: no split there.
-    if (!pv8) kv_split_plan(int64_t(units), d->tokens, d->causal, &kv_chunk, &nchunk);
+    // quant.hpp:258-279), so chunked maxima would change its codes: no split there.  The
+    // binary16 accumulator arm keeps one accumulator per row over all keys: no split either.
+    if (!pv8 && d->pv_accum == SAB_PV_FP32) kv_split_plan(int64_t(units), d->tokens, d->causal, &kv_chunk, &nchunk);
     const size_t npair = (size_t(d->tokens) + 2 * kBlockQ - 1) / (2 * kBlockQ);
     const size_t items = kv_chunk ? units * npair * size_t(nchunk) : 0;
     // Everything a call must find zeroed is contiguous (one memset per call, see
@@ -142,6 +143,7 @@ AttnParams attn_params(const sab_desc* d, const sab_ws_layout& L, const void* ws
     }
     a.o = o;
     a.o_v8 = (reinterpret_cast<uintptr_t>(o) & 31u) == 0;
+    a.pv16 = !pv8 && d->pv_accum == SAB_PV_FP16;
     a.status = at<int>(w, L.status);
     a.sched = a.status + 1;
     a.units = int(units_of(d));
@@ -266,8 +268,11 @@ int sab_check_desc(const sab_desc* d) {
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: P~V path must be FP16 (B/T) or INT8 (vB/vT)");
     if ((d->in_dtype != SAB_F16 && d->in_dtype != SAB_F32) || (d->out_dtype != SAB_F16 && d->out_dtype != SAB_F32))
         return set_error(SAB_ERR_ARGUMENT, "sab_desc: dtype must be SAB_F16 or SAB_F32");
-    if (d->pv_accum != SAB_PV_FP32)
-        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: only the FP32-accumulator P~V arm is implemented");
+    if (d->pv_accum != SAB_PV_FP32 && d->pv_accum != SAB_PV_FP16)
+        return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: P~V accumulator must be SAB_PV_FP32 or SAB_PV_FP16");
+    if (d->pv_accum == SAB_PV_FP16 && d->pv_path != SAB_PV_PATH_FP16)
+        return set_error(SAB_ERR_UNSUPPORTED,
+                         "sage_attention: the binary16 P~V accumulator applies to the FP16 P~V path (B/T)");
     if (units_of(d) > (int64_t(1) << 24))
         return set_error(SAB_ERR_UNSUPPORTED, "sage_attention: batch*heads too large");
     // The INT8 P~V path accumulates P~^ V^ in one INT32 TMEM accumulator per row over all

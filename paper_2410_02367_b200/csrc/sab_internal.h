@@ -86,6 +86,7 @@ struct AttnParams {
     // done) in the status block; persist == 0: one CTA per item.
     int items, persist;
     int o_v8;  // O is 32-byte aligned: the epilogue writes with 32-byte stores
+    int pv16;  // SAB_PV_FP16: P~V accumulates in a binary16 TMEM accumulator (never KV-split)
     int* sched;
     float* part_o;          // [units][npair][nchunk][d/4][256] float4 groups of unnormalised partial O
     float2* part_ml;        // [units][npair][nchunk][256] (m, l)

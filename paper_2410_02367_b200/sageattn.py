@@ -138,14 +138,30 @@ def _check_b_path(config: KernelConfig, options: SageOptions):
         raise ValueError("sage_attention: only INT8 P~V quantization runs on the B200 path")
 
 
+PV_ACCUM = {"fp32": _lib.SAB_PV_FP32, "fp16": _lib.SAB_PV_FP16}
+
+
+def _pv_accum(pv_accum: str) -> int:
+    if pv_accum not in PV_ACCUM:
+        raise ValueError("pv_accum must be 'fp32' or 'fp16'")
+    return PV_ACCUM[pv_accum]
+
+
 def sage_attention(inp: AttentionInput, config: Union[KernelConfig, SageVariant],
-                   options: Optional[SageOptions] = None, devices: Optional[Sequence[int]] = None) -> np.ndarray:
+                   options: Optional[SageOptions] = None, devices: Optional[Sequence[int]] = None,
+                   pv_accum: str = "fp32") -> np.ndarray:
     """SAGEAttn-B / -T / -vB / -vT forward on host arrays (B, H, N, d); returns float32 (B, H, N, d).
 
     Q/K/V may be float32 (bit-exact prepass for any finite float32 input) or
-    float16.  The P~V product always accumulates in FP32 on B200 (the
-    reference's ``pv_fp32_accumulator`` arm, attention.hpp:454-471)."""
+    float16.  pv_accum (B/T): "fp32" -- P~V accumulates in FP32 on B200 whatever
+    ``options.pv_fp32_accumulator`` says (the reference's FP32 arm,
+    attention.hpp:454-471; the parity gate); "fp16" -- a persistent binary16 TMEM
+    accumulator (the reference's default arm's semantics, attention.hpp:447-475);
+    "options" -- follow ``options.pv_fp32_accumulator`` as the reference does."""
     options = options or SageOptions()
+    if pv_accum == "options":
+        pv_accum = "fp32" if options.pv_fp32_accumulator else "fp16"
+    acc = _pv_accum(pv_accum)
     if isinstance(config, SageVariant):
         config = kernel_config_for(config)
     _check_b_path(config, options)
@@ -164,7 +180,8 @@ def sage_attention(inp: AttentionInput, config: Union[KernelConfig, SageVariant]
                          out_dtype=_lib.SAB_F32, block_q=config.block_q, block_kv=config.block_kv,
                          smooth_k=options.smooth_k, check_v=True,
                          per_token=config.qk_granularity == QkGranularity.PerToken,
-                         pv_int8=config.pv_path == PvPath.Int8)
+                         pv_int8=config.pv_path == PvPath.Int8,
+                         pv_accum=acc if config.pv_path == PvPath.Fp16Acc else _lib.SAB_PV_FP32)
         diag = options.diagnostics
         desc.measure_static_scale = int(diag is not None and diag.measure_static_scale
                                         and config.pv_path == PvPath.Int8)
@@ -225,13 +242,13 @@ def _stream_ptr(stream) -> int:
 
 
 def make_desc(q, causal: bool, out_dtype=None, smooth_k: bool = True, check_v: bool = False,
-              per_token: bool = False, pv_int8: bool = False) -> _lib.SabDesc:
+              per_token: bool = False, pv_int8: bool = False, pv_accum: str = "fp32") -> _lib.SabDesc:
     torch = _torch()
     b, h, n, d = q.shape
     in_dt = _lib.SAB_F16 if q.dtype == torch.float16 else _lib.SAB_F32
     out_dt = _lib.SAB_F32 if out_dtype == torch.float32 else _lib.SAB_F16
     return _lib.desc(b, h, n, d, causal, in_dtype=in_dt, out_dtype=out_dt, smooth_k=smooth_k, check_v=check_v,
-                     per_token=per_token, pv_int8=pv_int8)
+                     per_token=per_token, pv_int8=pv_int8, pv_accum=_pv_accum(pv_accum))
 
 
 ROPE_LAYOUTS = {"interleaved": _lib.SAB_ROPE_INTERLEAVED, "half": _lib.SAB_ROPE_HALF}
@@ -297,7 +314,7 @@ def read_status(ws: Workspace, stream=None) -> int:
 
 def sage_attention_cuda(q, k, v, causal: bool = False, out=None, out_dtype=None, smooth_k: bool = True,
                         ws: Optional[Workspace] = None, stream=None, check: bool = True, per_token: bool = False,
-                        pv_int8: bool = False, rope=None):
+                        pv_int8: bool = False, rope=None, pv_accum: str = "fp32"):
     """K1 + K2 on device-resident CUDA tensors (B,H,N,d); returns O (fp16 by default).
 
     With check=True the stream is synchronised and data-dependent errors raise
@@ -305,7 +322,8 @@ def sage_attention_cuda(q, k, v, causal: bool = False, out=None, out_dtype=None,
     rope = (cos, sin, layout): Q and K are the pre-rotation tensors, rotated inside K1."""
     torch = _torch()
     out_dtype = out_dtype or (out.dtype if out is not None else torch.float16)
-    desc = make_desc(q, causal, out_dtype=out_dtype, smooth_k=smooth_k, per_token=per_token, pv_int8=pv_int8)
+    desc = make_desc(q, causal, out_dtype=out_dtype, smooth_k=smooth_k, per_token=per_token, pv_int8=pv_int8,
+                     pv_accum=pv_accum)
     if ws is None or ws.nbytes < int(_lib.workspace_layout(desc).total):
         ws = Workspace(desc, q.device)
     ws.desc = desc
@@ -345,12 +363,14 @@ def qk_int32_tiles_cuda(ws: Workspace, unit: int, q_tile: int, stream=None):
 
 
 def attention_fwd_host(q: np.ndarray, k: np.ndarray, v: np.ndarray, causal: bool, out: np.ndarray,
-                       devices: Sequence[int] = (0,), per_token: bool = False, pv_int8: bool = False):
+                       devices: Sequence[int] = (0,), per_token: bool = False, pv_int8: bool = False,
+                       pv_accum: str = "fp32"):
     """The C-ABI host-buffer call (sab_attention_fwd_host) on raw fp16/fp32 arrays; `out` receives O."""
     b, h, n, d = q.shape
     in_dt = _lib.SAB_F16 if q.dtype == np.float16 else _lib.SAB_F32
     out_dt = _lib.SAB_F16 if out.dtype == np.float16 else _lib.SAB_F32
-    desc = _lib.desc(b, h, n, d, causal, in_dtype=in_dt, out_dtype=out_dt, per_token=per_token, pv_int8=pv_int8)
+    desc = _lib.desc(b, h, n, d, causal, in_dtype=in_dt, out_dtype=out_dt, per_token=per_token, pv_int8=pv_int8,
+                     pv_accum=_pv_accum(pv_accum))
     arr = (C.c_int * len(devices))(*devices)
     try:
         _lib.check(_lib.load().sab_attention_fwd_host(C.byref(desc), q.ctypes.data, k.ctypes.data, v.ctypes.data,

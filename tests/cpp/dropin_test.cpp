@@ -61,6 +61,17 @@ int main(int argc, char** argv) {
     const sageattn::Tensor4f out_vt = sageattn::sage_attention(in, sageattn::SageVariant::VT);
     std::ofstream(std::string(argv[9]) + ".vt", std::ios::binary)
         .write(reinterpret_cast<const char*>(out_vt.data.data()), std::streamsize(out_vt.size() * sizeof(float)));
+    // The reference's own option mapping: pv_fp32_accumulator == false (the default) selects
+    // the binary16 P~V accumulator, true the FP32 one.
+    sageattn::b200::honour_pv_accumulator_option() = true;
+    const sageattn::Tensor4f out_16 = sageattn::sage_attention(in, sageattn::SageVariant::B);
+    sageattn::SageOptions o32;
+    o32.pv_fp32_accumulator = true;
+    const sageattn::Tensor4f out_32 = sageattn::sage_attention(in, sageattn::SageVariant::B, o32);
+    sageattn::b200::honour_pv_accumulator_option() = false;
+    std::ofstream(std::string(argv[9]) + ".f16", std::ios::binary)
+        .write(reinterpret_cast<const char*>(out_16.data.data()), std::streamsize(out_16.size() * sizeof(float)));
+    std::printf("PV32 SAME %d\n", out_32.data == out.data ? 1 : 0);
     std::printf("MACS %llu %llu\n", (unsigned long long)diag.s_stage_macs, (unsigned long long)diag.pv_stage_macs);
     // Static-scale P~ diagnostics of the INT8 P~V path (attention.hpp:479-488).
     sageattn::SageDiagnostics sdiag;

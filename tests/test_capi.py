@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.sab_abi_version() == 6
+    assert lib.sab_abi_version() == 7
 
 
 def test_desc_validation_mirrors_reference():
@@ -33,8 +33,15 @@ def test_desc_validation_mirrors_reference():
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 0, 1024, 64))) == _lib.SAB_ERR_SHAPE
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 96))) == _lib.SAB_ERR_UNSUPPORTED
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, block_q=64))) == _lib.SAB_ERR_UNSUPPORTED
-    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=1))) == \
+    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=_lib.SAB_PV_FP16))) == _lib.SAB_OK
+    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=2))) == _lib.SAB_ERR_UNSUPPORTED
+    # the binary16 accumulator belongs to the FP16 P~V path (B/T), not to vB/vT
+    assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, pv_accum=_lib.SAB_PV_FP16, pv_int8=True))) == \
         _lib.SAB_ERR_UNSUPPORTED
+    # ... and never takes the KV split (one accumulator per row over all keys)
+    few = _lib.desc(1, 1, 16384, 128, pv_accum=_lib.SAB_PV_FP16)
+    assert _lib.workspace_layout(few).kv_chunk == 0
+    assert _lib.workspace_layout(_lib.desc(1, 1, 16384, 128)).kv_chunk > 0
     assert lib.sab_check_desc(C.byref(_lib.desc(1, 1, 1024, 64, per_token=True))) == _lib.SAB_OK
     assert lib.sab_check_desc(C.byref(_lib.desc(2, 32768, 64, 64))) == _lib.SAB_OK  # host path chunks it
     bad_g = _lib.desc(1, 1, 1024, 64)

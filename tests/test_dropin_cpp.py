@@ -67,6 +67,13 @@ def test_dropin_runs_on_b200(tmp_path, cuda, oracle, shape, causal):
                                                                causal)
         assert el == r_el
         assert abs(first - r_first) <= max(2, 0.01 * r_first) and abs(later - r_later) <= max(2, 0.01 * r_later)
+    # honour_pv_accumulator_option(): the default options select the binary16 accumulator
+    # (tests/test_gpu_pv16.py's gate), pv_fp32_accumulator=true the FP32 arm above.
+    assert "PV32 SAME 1" in r.stdout
+    o_16 = np.fromfile(str(out) + ".f16", np.float32).reshape(b * h, n, d)
+    ref16, _ = oracle.sage_b(q, k, v, causal, pv_fp32=False)
+    drift = relative_l1(ref16, ref)
+    assert relative_l1(o_16, ref) <= drift and relative_l1(o_16, ref16) <= 1.5 * drift
     o_t = np.fromfile(str(out) + ".t", np.float32).reshape(b * h, n, d)
     ref_t, _ = oracle.sage(q, k, v, causal, pv_fp32=True, per_token=True)
     assert cosine_sim(o_t, ref_t) >= 0.9999 and relative_l1(o_t, ref_t) <= 2e-3
