@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -456,7 +457,8 @@ namespace {
 // never share buffers (the reference entry is re-entrant, attention.hpp:9-12).
 struct DevCtx {
     int device = -1;
-    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaStream_t s_cmp[2] = {nullptr, nullptr};  // chunks alternate: adjacent chunks' kernels overlap
     std::vector<cudaEvent_t> ev_in, ev_cmp, ev_out;
     uint8_t* buf = nullptr;
     size_t buf_bytes = 0;
@@ -472,7 +474,8 @@ cudaError_t ctx_reserve(DevCtx* c, size_t bytes, int n_events) {
     cudaError_t e = cudaSuccess;
     if (!c->s_in) {
         if ((e = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->s_cmp[0], cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&c->s_cmp[1], cudaStreamNonBlocking)) != cudaSuccess ||
             (e = cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking)) != cudaSuccess)
             return e;
     }
@@ -585,20 +588,63 @@ struct ShardJob {
     unsigned long long mismatches[2] = {0, 0};  // static-scale P~ diagnostics of this shard
 };
 
+// Test / tuning knobs of the host-buffer path (read once): SAB_HOST_CHUNK_UNITS forces
+// the units per (full) chunk, SAB_HOST_RAMP=0 turns the size ramp off, SAB_HOST_STREAMS=1
+// keeps every chunk on one compute stream.
+int host_chunk_units() {
+    static const int v = [] {
+        const char* e = std::getenv("SAB_HOST_CHUNK_UNITS");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+int host_ramp() {
+    static const int v = [] {
+        const char* e = std::getenv("SAB_HOST_RAMP");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+int host_compute_streams() {
+    static const int v = [] {
+        const char* e = std::getenv("SAB_HOST_STREAMS");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    return v;
+}
+
 int run_shard_on(ShardJob* job, DevCtx* ctx) {
     const sab_desc* D = job->desc;
     const size_t in_e = elem_size(D->in_dtype), out_e = elem_size(D->out_dtype);
     const size_t unit_elems = size_t(D->tokens) * D->head_dim;
-    // Chunks of whole units (~24 MB of inputs, and at least ~8 chunks when the
-    // shard allows) so that H2D of chunk c+1, compute of chunk c and D2H of chunk
-    // c-1 overlap on the three streams; small chunks shorten the un-overlapped
-    // first H2D and last D2H.
+    // Chunks of whole units (up to ~128 MB of inputs, and at least ~4 full chunks when
+    // the shard allows) so that H2D of chunk c+1, compute of chunk c and D2H of chunk
+    // c-1 overlap on the three streams.  The sizes ramp 1, 2, 4, ... units up to that
+    // and back down at the end: the un-overlapped first H2D and last compute + D2H
+    // are one unit's worth, while the middle chunks are large enough that per-copy
+    // overheads and partial K2 waves stay small.
     const size_t unit_in_bytes = 3 * unit_elems * in_e;
-    const size_t by_bytes = std::max<size_t>(1, (24u << 20) / unit_in_bytes);
-    const size_t by_count = std::max<size_t>(1, size_t(job->count) / 8);
-    const int chunk = int(std::max<size_t>(
+    const size_t by_bytes = std::max<size_t>(1, (128u << 20) / unit_in_bytes);
+    const size_t by_count = std::max<size_t>(1, size_t(job->count) / 4);
+    int chunk = int(std::max<size_t>(
         1, std::min<size_t>(std::min<size_t>(job->count, size_t(kMaxUnitsPerLaunch)), std::min(by_bytes, by_count))));
-    const int n_chunks = (job->count + chunk - 1) / chunk;
+    if (const int forced = host_chunk_units(); forced > 0)
+        chunk = std::min(std::min(forced, job->count), int(kMaxUnitsPerLaunch));
+    std::vector<int> starts{0};
+    {
+        std::vector<int> up;
+        int ramp = 0;
+        if (host_ramp())
+            for (int sz = 1; sz < chunk && 2 * (ramp + sz) + chunk <= job->count; sz *= 2) up.push_back(sz), ramp += sz;
+        auto push = [&](int sz) { starts.push_back(starts.back() + sz); };
+        for (int sz : up) push(sz);
+        for (int rem = job->count - 2 * ramp; rem > 0; rem -= std::min(chunk, rem)) push(std::min(chunk, rem));
+        for (auto it = up.rbegin(); it != up.rend(); ++it) push(*it);
+    }
+    const int n_chunks = int(starts.size()) - 1;
+    // Chunks alternate between two compute streams, each with its own workspace, so the
+    // tail wave of chunk c's K2 overlaps chunk c+1's K1 and first wave.
+    const int ncs = (n_chunks > 1 && host_compute_streams() > 1) ? 2 : 1;
 
     sab_desc cd = *D;
     cd.batch = 1;
@@ -608,7 +654,8 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
 
     const size_t in_bytes = align_up(size_t(job->count) * unit_elems * in_e, 256);
     const size_t out_bytes = align_up(size_t(job->count) * unit_elems * out_e, 256);
-    cudaError_t e = ctx_reserve(ctx, 3 * in_bytes + out_bytes + L.total, n_chunks);
+    const size_t ws_bytes = align_up(L.total, 256);
+    cudaError_t e = ctx_reserve(ctx, 3 * in_bytes + out_bytes + ncs * ws_bytes, n_chunks);
     if (e != cudaSuccess) return cuda_fail(e, "sab_attention_fwd_host: device buffers");
     // Pageable caller buffers go through two pinned slots per direction: the host
     // thread copies chunk c into slot c % 2 while the GPU reads chunk c - 1 from the
@@ -624,13 +671,14 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     }
     uint8_t* dev_in[3] = {ctx->buf, ctx->buf + in_bytes, ctx->buf + 2 * in_bytes};
     uint8_t* dout = ctx->buf + 3 * in_bytes;
-    uint8_t* ws = dout + out_bytes;
+    uint8_t* wss[2] = {dout + out_bytes, dout + out_bytes + ws_bytes};
 
-    if ((e = cudaMemsetAsync(ws + L.status, 0, reset_bytes(L), ctx->s_cmp)) != cudaSuccess)
-        return cuda_fail(e, "sab_attention_fwd_host: memset");
+    for (int i = 0; i < ncs; ++i)
+        if ((e = cudaMemsetAsync(wss[i] + L.status, 0, reset_bytes(L), ctx->s_cmp[i])) != cudaSuccess)
+            return cuda_fail(e, "sab_attention_fwd_host: memset");
     // Copies the finished O of chunk c out of its pinned slot into the caller's buffer.
     auto drain_out = [&](int c) -> cudaError_t {
-        const int u0 = c * chunk, cu = std::min(chunk, job->count - u0);
+        const int u0 = starts[c], cu = starts[c + 1] - starts[c];
         cudaError_t x = cudaEventSynchronize(ctx->ev_out[c]);
         if (x == cudaSuccess)
             par_copy(job->o + size_t(u0) * unit_elems * out_e, ctx->pin_out[c % 2], size_t(cu) * unit_elems * out_e,
@@ -639,10 +687,12 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     };
     int st = SAB_OK;
     for (int c = 0; c < n_chunks && st == SAB_OK; ++c) {
-        const int u0 = c * chunk, cu = std::min(chunk, job->count - u0);
+        const int u0 = starts[c], cu = starts[c + 1] - starts[c];
         const size_t ioff = size_t(u0) * unit_elems * in_e, ibytes = size_t(cu) * unit_elems * in_e;
         const size_t ooff = size_t(u0) * unit_elems * out_e, obytes = size_t(cu) * unit_elems * out_e;
         const int slot = c % 2;
+        cudaStream_t scmp = ctx->s_cmp[c % ncs];
+        uint8_t* ws = wss[c % ncs];
         // The slot was last read by the H2D of chunk c - 2.
         if (any_in && c >= 2 && (e = cudaEventSynchronize(ctx->ev_in[c - 2])) != cudaSuccess) {
             st = cuda_fail(e, "sab_attention_fwd_host: staging");
@@ -658,7 +708,7 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
             e = cudaMemcpyAsync(dev_in[t] + ioff, from, ibytes, cudaMemcpyHostToDevice, ctx->s_in);
         }
         if (e != cudaSuccess || (e = cudaEventRecord(ctx->ev_in[c], ctx->s_in)) != cudaSuccess ||
-            (e = cudaStreamWaitEvent(ctx->s_cmp, ctx->ev_in[c], 0)) != cudaSuccess) {
+            (e = cudaStreamWaitEvent(scmp, ctx->ev_in[c], 0)) != cudaSuccess) {
             st = cuda_fail(e, "sab_attention_fwd_host: H2D");
             break;
         }
@@ -668,12 +718,12 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
         // (V^ / delta_V of the INT8 P~V path) on top of it.
         sab_desc xd = cd;
         xd.heads = cu;
-        if ((st = enqueue_prepass(&xd, L, dev_in[0] + ioff, dev_in[1] + ioff, dev_in[2] + ioff, ws, ctx->s_cmp,
-                                  false)) != SAB_OK)
+        if ((st = enqueue_prepass(&xd, L, dev_in[0] + ioff, dev_in[1] + ioff, dev_in[2] + ioff, ws, scmp, false)) !=
+            SAB_OK)
             break;
-        if ((st = enqueue_attention(&xd, L, ws, dev_in[2] + ioff, dout + ooff, ctx->s_cmp)) != SAB_OK) break;
+        if ((st = enqueue_attention(&xd, L, ws, dev_in[2] + ioff, dout + ooff, scmp)) != SAB_OK) break;
         // The O slot of chunk c was last filled by chunk c - 2, drained below at step c - 1.
-        if ((e = cudaEventRecord(ctx->ev_cmp[c], ctx->s_cmp)) != cudaSuccess ||
+        if ((e = cudaEventRecord(ctx->ev_cmp[c], scmp)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(ctx->s_out, ctx->ev_cmp[c], 0)) != cudaSuccess ||
             (e = cudaMemcpyAsync(stage_out ? ctx->pin_out[slot] : job->o + ooff, dout + ooff, obytes,
                                  cudaMemcpyDeviceToHost, ctx->s_out)) != cudaSuccess ||
@@ -688,21 +738,27 @@ int run_shard_on(ShardJob* job, DevCtx* ctx) {
     }
     if (st == SAB_OK && stage_out && (e = drain_out(n_chunks - 1)) != cudaSuccess)
         st = cuda_fail(e, "sab_attention_fwd_host: D2H staging");
-    int word = 0;
-    if (st == SAB_OK &&
-        (e = cudaMemcpyAsync(&word, ws + L.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->s_cmp)) != cudaSuccess)
-        st = cuda_fail(e, "sab_attention_fwd_host: status");
-    if (st == SAB_OK && D->measure_static_scale &&
-        (e = cudaMemcpyAsync(job->mismatches, ws + L.diag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                             ctx->s_cmp)) != cudaSuccess)
-        st = cuda_fail(e, "sab_attention_fwd_host: diagnostics");
-    // Always drain all three streams before the context is reused.
-    cudaError_t e1 = cudaStreamSynchronize(ctx->s_in), e2 = cudaStreamSynchronize(ctx->s_cmp),
-                e3 = cudaStreamSynchronize(ctx->s_out);
+    int word[2] = {0, 0};
+    unsigned long long mism[2][2] = {{0, 0}, {0, 0}};
+    for (int i = 0; i < ncs && st == SAB_OK; ++i) {
+        if ((e = cudaMemcpyAsync(&word[i], wss[i] + L.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->s_cmp[i])) !=
+            cudaSuccess)
+            st = cuda_fail(e, "sab_attention_fwd_host: status");
+        else if (D->measure_static_scale &&
+                 (e = cudaMemcpyAsync(mism[i], wss[i] + L.diag, sizeof(mism[i]), cudaMemcpyDeviceToHost,
+                                      ctx->s_cmp[i])) != cudaSuccess)
+            st = cuda_fail(e, "sab_attention_fwd_host: diagnostics");
+    }
+    // Always drain every stream before the context is reused.
+    cudaError_t es[4] = {cudaStreamSynchronize(ctx->s_in), cudaStreamSynchronize(ctx->s_cmp[0]),
+                         cudaStreamSynchronize(ctx->s_cmp[1]), cudaStreamSynchronize(ctx->s_out)};
     if (st == SAB_OK) {
-        e = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3);
-        if (e != cudaSuccess) return cuda_fail(e, "sab_attention_fwd_host: sync");
-        st = map_status_word(word);
+        for (cudaError_t x : es)
+            if (x != cudaSuccess) return cuda_fail(x, "sab_attention_fwd_host: sync");
+        job->mismatches[0] = mism[0][0] + mism[1][0];
+        job->mismatches[1] = mism[0][1] + mism[1][1];
+        st = map_status_word(word[0]);
+        if (st == SAB_OK) st = map_status_word(word[1]);
     }
     return st;
 }
