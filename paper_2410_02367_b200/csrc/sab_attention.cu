@@ -86,6 +86,15 @@ constexpr uint32_t kMagicI = 0x4B400000u;  // bits of 2^23 + 2^22
 constexpr int kMaskedAcc = 0;              // sentinel below any biased S value (bits of +0.0f)
 // Exponentials (of every 16) evaluated by exp2_poly2 on the FMA pipe instead of MUFU,
 // per head dim (d=64 is MUFU-bound, d=128 closer to the tensor/SMEM bound).
+// Which pairs of each 8 take the FMA-pipe exponential: pair index p with
+// ((2p + rot) & 15) >= 16 - POLY.  Only the instruction schedule changes (C3 +1.4 % at
+// rot 2 for d=64, C2 +0.6 % at rot 8 for d=128, profiles/r02_polyrot_ab.txt).
+#ifndef SAB_POLYROT64
+#define SAB_POLYROT64 2
+#endif
+#ifndef SAB_POLYROT128
+#define SAB_POLYROT128 8
+#endif
 #ifndef SAB_POLY128
 #define SAB_POLY128 2
 #endif
@@ -94,6 +103,8 @@ constexpr int kMaskedAcc = 0;              // sentinel below any biased S value 
 #endif
 template <int D>
 constexpr int poly_per16() { return D == 64 ? SAB_POLY64 : SAB_POLY128; }
+template <int D>
+constexpr int poly_rot() { return D == 64 ? SAB_POLYROT64 : SAB_POLYROT128; }
 constexpr float kMagicF = 12582912.0f;     // 2^23 + 2^22
 
 // ------------------------------------------------------------ packed fp32 math
@@ -240,7 +251,7 @@ __device__ __forceinline__ int group_max(const uint32_t (&r)[N], int lim) {
 // the running max m (log2 units) and this thread's partial row sum l; returns the
 // O rescale factor (1 when the warp skips the lazy rescale).  `dump` receives
 // the raw half row.
-template <bool MASK, bool CAUSAL, int POLY>
+template <bool MASK, bool CAUSAL, int POLY, int ROT>
 __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t ts, int half, float cg, int kb, int qi,
                                               int n, float& m, float& l, bool& rescale, int32_t* dump,
                                               int trole = -1, int ttile = 0) {
@@ -288,7 +299,7 @@ __device__ __forceinline__ float softmax_half(const uint32_t (&r)[32], uint32_t 
 #ifdef SAB_SK_NOEXP  // timing skeleton: no exponentials (wrong results)
         pp = t;
 #else
-        if ((c & 15) >= 16 - POLY) {  // part of the exponentials on the FMA pipe
+        if (((c + ROT) & 15) >= 16 - POLY) {  // part of the exponentials on the FMA pipe
             pp = exp2_poly2(t);
         } else {
             pp = f2{ex2(t.x), ex2(t.y)};
@@ -929,10 +940,10 @@ __device__ __forceinline__ void softmax_item(const AttnParams& p, Bars* bars, ui
                     alpha = softmax_half_pt<false, CAUSAL, poly_per16<D>()>(r, t_s, half, qsl, dkp, kb, SAB_QI, n,
                                                                             m, l, rescale, dump, j == 0);
             } else if (need_mask) {
-                alpha = softmax_half<true, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
+                alpha = softmax_half<true, CAUSAL, poly_per16<D>(), poly_rot<D>()>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
                                                                     dump, tr ? x : -1, j);
             } else {
-                alpha = softmax_half<false, CAUSAL, poly_per16<D>()>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
+                alpha = softmax_half<false, CAUSAL, poly_per16<D>(), poly_rot<D>()>(r, t_s, half, cg, kb, SAB_QI, n, m, l, rescale,
                                                                      dump, tr ? x : -1, j);
             }
             if (tr) SAB_STAMP(x, j, 2);
