@@ -598,6 +598,15 @@ int host_chunk_units() {
     }();
     return v;
 }
+// Host threads per staging copy of a shard: SAB_HOST_COPY_THREADS, else up to 8 per device.
+int host_copy_threads(int n_devices) {
+    static const int forced = [] {
+        const char* e = std::getenv("SAB_HOST_COPY_THREADS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return forced;
+    return std::max(1, std::min(8, int(std::thread::hardware_concurrency()) / std::max(1, n_devices)));
+}
 int host_ramp() {
     static const int v = [] {
         const char* e = std::getenv("SAB_HOST_RAMP");
@@ -826,7 +835,7 @@ int sab_attention_fwd_host_diag(const sab_desc* d, const void* q, const void* k,
         j.k = static_cast<const uint8_t*>(k) + j.first * in_unit;
         j.v = static_cast<const uint8_t*>(v) + j.first * in_unit;
         j.o = static_cast<uint8_t*>(o) + j.first * out_unit;
-        j.copy_threads = std::max(1, std::min(8, int(std::thread::hardware_concurrency()) / n_devices));
+        j.copy_threads = host_copy_threads(n_devices);
         j.status = SAB_OK;
     }
     if (n_devices == 1) {
