@@ -331,8 +331,10 @@ def dropin_e2e(hq, hk, hv, wl, batch, iters: int):
                                                                          ctypes.c_void_p]
     q32, k32, v32 = (np.ascontiguousarray(x, dtype=np.float32) for x in (hq, hk, hv))
     sec = ctypes.c_double()
-    st = lib.sab_dropin_bench(q32, k32, v32, batch, wl["heads"], wl["tokens"], wl["head_dim"], int(wl["causal"]),
-                              iters, ctypes.byref(sec), None)
+    # The host arrays hold this rank's (or --shard-of's) units: (1, count, n, d), not the workload's (B, H).
+    b, h, n, d = q32.shape
+    assert (n, d) == (wl["tokens"], wl["head_dim"])
+    st = lib.sab_dropin_bench(q32, k32, v32, b, h, n, d, int(wl["causal"]), iters, ctypes.byref(sec), None)
     if st != 0:
         return {"error": "sab_dropin_bench failed"}
     nbytes = q32.nbytes

@@ -71,7 +71,9 @@ int layout_of(const sab_desc* d, sab_ws_layout* L) {
     const size_t items = kv_chunk ? units * npair * size_t(nchunk) : 0;
     // Everything a call must find zeroed is contiguous (one memset per call, see
     // reset_bytes): status word + per-unit K1 counters, static-scale counters, split counters.
-    L->status = take(sizeof(int32_t) * (3 + units));  // word, K2 scheduler [2], K1 per-unit counters
+    // word, K2 scheduler [2], K1 per-unit counters [3 x units] (mean partials done, mean ready,
+    // K chunks past the mean wait) and K1's ticket counter.
+    L->status = take(sizeof(int32_t) * (4 + 3 * units));
     L->diag = take(2 * sizeof(unsigned long long));
     L->split_cnt = take(kv_chunk ? 2 * units * npair * sizeof(int32_t) : 0);
     L->vcodes = take(pv8 ? units * hd * npad : 0);
@@ -113,6 +115,9 @@ PrepassParams prepass_params(const sab_desc* d, const sab_ws_layout& L, const vo
     }
     p.status = at<int>(ws, L.status);
     p.counters = p.status + 3;
+    p.ready = p.counters + units_of(d);
+    p.kdone = p.ready + units_of(d);
+    p.ticket = p.kdone + units_of(d);
     p.units = int(units_of(d));
     p.n = d->tokens;
     p.d = d->head_dim;

@@ -34,6 +34,10 @@ struct PrepassParams {
     uint16_t* v16;
     int* status;
     int* counters;      // per unit: mean-partial CTAs done (self-resetting, zeroed with status)
+    int* ready;         // per unit: mean(K) written (k1_fused; self-resetting)
+    int* kdone;         // per unit: K chunks past their mean(K) wait (k1_fused; self-resetting)
+    int* ticket;        // k1_fused: next work-item ticket (self-resetting)
+    int lag;            // k1_fused: K chunks of unit u are issued in stage u + lag
     int units, n, d;
     int depth;          // tree depth of the 4..9-token node level
     int nodes_per_cta;  // nodes summed per mean-partial CTA (power of two)

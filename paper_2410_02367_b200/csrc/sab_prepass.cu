@@ -30,6 +30,7 @@
 // __float2int_rn reproduce the reference's binary32 operations one for one.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -234,7 +235,21 @@ __device__ __forceinline__ void mean_top(const PrepassParams& p, int unit, int c
     p.mean[static_cast<size_t>(unit) * D + c] = __fmul_rn(stk[0], p.inv_n);
 }
 
-template <typename T, int D, int G>
+// k1_fused's per-unit "mean(K) written" flag: release by the CTA that wrote mean_k,
+// acquire by the K chunks of the unit.
+__device__ __forceinline__ void flag_release(int* f) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+}
+__device__ __forceinline__ void flag_wait(const int* f) {
+    for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) return;
+        __nanosleep(128);
+    }
+}
+
+template <typename T, int D, int G, bool FLAG = false>
 __device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, int chunk) {
     constexpr int CV = D / 8;           // 8-channel vectors per row
     constexpr int NG = kThreads / CV;   // node groups per CTA
@@ -306,6 +321,11 @@ __device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, i
     if (s_last) {
         __threadfence();
         if (threadIdx.x < D) mean_top<D>(p, unit, threadIdx.x);
+        if constexpr (FLAG) {  // s_last is CTA-uniform
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) flag_release(p.ready + unit);
+        }
     }
 }
 
@@ -791,17 +811,19 @@ __global__ void __launch_bounds__(kQThreads, SAB_K1_MINB) k1_mean_and_q(PrepassP
     else q_chunk_fast<D>(p, blockIdx.y, blockIdx.x - p.n_partials, smem);
 }
 
-template <int D>
-__global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
+// Smooth + quantize the two 64-token K groups of 128-token chunk `chunk`.  FUSED (k1_fused):
+// mean(K) is awaited through the unit's ready flag; else (k1_k_fast) through the PDL wait on
+// the k1_mean_and_q grid.
+template <int D, bool FUSED>
+__device__ __forceinline__ void k_chunk_fast(const PrepassParams& p, int unit, int chunk, uint8_t* smem) {
     constexpr int CV = D / 8;
     constexpr int VPT = kBlockQ * CV / kQThreads;
-    extern __shared__ __align__(128) uint8_t smem[];
     const __half* sk = reinterpret_cast<const __half*>(smem);
     __shared__ uint64_t bar;
     __shared__ float s_mean[D];
     __shared__ float s_red[kQThreads / 32][2];
     __shared__ float s_inv[2];
-    const int unit = blockIdx.y, chunk = blockIdx.x, tid = threadIdx.x;
+    const int tid = threadIdx.x;
     const int r0 = chunk * kBlockQ;
     const int rows = min(kBlockQ, p.n - r0);
     const size_t ubase = static_cast<size_t>(unit) * p.n * D;
@@ -813,11 +835,23 @@ __global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
         bulk_load(smem_u32(smem), static_cast<const __half*>(p.k) + ubase + static_cast<size_t>(r0) * D, bytes,
                   smem_u32(&bar));
     }
-    // K is an input: its load is in flight before mean(K) (k1_mean_and_q's output) is
-    // awaited.  Every CTA waits, so this grid never completes before its producer.
-    griddep_wait();
-    griddep_launch_dependents();  // K2 may be scheduled behind this grid's last wave
-    if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
+    // K is an input: its load is in flight before mean(K) is awaited.
+    if constexpr (FUSED) {
+        // Every ticket this chunk depends on (the unit's mean partials) is lower than its
+        // own, so those CTAs are already running: the wait cannot deadlock.
+        if (tid == 0) flag_wait(p.ready + unit);
+        __syncthreads();
+        if (tid == 0 && atomicAdd(p.kdone + unit, 1) == (p.n + kBlockQ - 1) / kBlockQ - 1) {
+            p.kdone[unit] = 0;  // every K chunk of the unit is past its wait: reset for the next call
+            p.ready[unit] = 0;
+        }
+        if (tid < D) s_mean[tid] = __ldcg(p.mean + static_cast<size_t>(unit) * D + tid);
+    } else {
+        // Every CTA waits, so this grid never completes before its producer.
+        griddep_wait();
+        griddep_launch_dependents();  // K2 may be scheduled behind this grid's last wave
+        if (tid < D) s_mean[tid] = p.smooth ? p.mean[static_cast<size_t>(unit) * D + tid] : 0.0f;
+    }
     __syncthreads();
     mbar_wait(smem_u32(&bar), 0);
     const int col = (tid % CV) * 8;
@@ -889,6 +923,57 @@ __global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
         }
         if (!vfin) atomicOr(p.status, kStatusNonFinite);
     }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    k_chunk_fast<D, false>(p, blockIdx.y, blockIdx.x, smem);
+}
+
+// ---- fp16, per-block path in ONE launch (opt-in experiment, SAB_K1_FUSED=1).  Each CTA
+// takes a ticket (atomic counter) and runs the work item of that ticket; items are ordered in stages, stage s = [mean partials of unit s][Q chunks of unit
+// s][K chunks of unit s - lag], so a K chunk waits (per-unit flag) only on CTAs with lower
+// tickets -- already running, so no deadlock -- and re-reads its K rows from L2 a few
+// units after the mean partials read them (lag ~ 1.5 resident waves of items): K comes
+// from DRAM once instead of twice, and there is no grid-wide dependency between K's mean
+// and its quantization.
+template <int D, int G>
+__global__ void __launch_bounds__(kQThreads, SAB_K1_MINB) k1_fused(PrepassParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ int s_ticket;
+    griddep_launch_dependents();  // K2 may be scheduled behind this grid's last wave
+    if (threadIdx.x == 0) {
+        const int t = atomicAdd(p.ticket, 1);
+        if (t == static_cast<int>(gridDim.x) - 1) *p.ticket = 0;  // every ticket is taken: reset
+        s_ticket = t;
+    }
+    __syncthreads();
+    const int t = s_ticket;
+    const int np = p.n_partials, nq = (p.n + kBlockQ - 1) / kBlockQ;
+    const int pq = np + nq, lag = p.lag;
+    const int t1 = lag * pq, t2 = t1 + (p.units - lag) * (pq + nq);
+    int unit, r;
+    bool kchunk;
+    if (t < t1) {
+        unit = t / pq;
+        r = t - unit * pq;
+        kchunk = false;
+    } else if (t < t2) {
+        const int tt = t - t1, st = tt / (pq + nq);
+        r = tt - st * (pq + nq);
+        kchunk = r >= pq;
+        unit = kchunk ? st : st + lag;
+        if (kchunk) r -= pq;
+    } else {
+        const int tt = t - t2, st = tt / nq;
+        unit = p.units - lag + st;
+        r = tt - st * nq;
+        kchunk = true;
+    }
+    if (kchunk) k_chunk_fast<D, true>(p, unit, r, smem);
+    else if (r < np) mean_partial<__half, D, G, true>(p, unit, r);
+    else q_chunk_fast<D>(p, unit, r - np, smem);
 }
 
 // ---------------------------------------------------------------- vB: V^ per channel
@@ -1002,9 +1087,54 @@ bool k1_alt(const PrepassParams& p) {
     return mode >= 0 ? mode == 1 : p.units <= 8;
 }
 
+// SAB_K1_FUSED=1 selects k1_fused (measured slower than the two launches, see
+// profiles/r02_experiments.md); SAB_K1_LAG_PCT sets its stage lag in percent of one resident
+// wave of CTAs (default 150).
+bool k1_fused_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("SAB_K1_FUSED");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+template <int D, int G>
+cudaError_t launch_k1_fused(PrepassParams p, cudaStream_t s) {
+    constexpr int smem = kBlockQ * D * 2;
+    static int resident = 0;  // CTAs of k1_fused resident on the device at once
+    cudaError_t e;
+    if (resident == 0) {
+        if ((e = cudaFuncSetAttribute(k1_fused<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
+            return e;
+        int dev = 0, sms = 0, per_sm = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
+            (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess ||
+            (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_fused<D, G>, kQThreads, smem)) !=
+                cudaSuccess)
+            return e;
+        resident = std::max(1, sms * per_sm);
+    }
+    static const int pct = [] {
+        const char* e = std::getenv("SAB_K1_LAG_PCT");
+        return e ? std::max(0, std::atoi(e)) : 150;
+    }();
+    const int nq = (p.n + kBlockQ - 1) / kBlockQ;
+    const long long per_stage = p.n_partials + 2LL * nq;
+    const long long lag_items = static_cast<long long>(resident) * pct / 100;
+    p.lag = static_cast<int>(std::min<long long>(p.units, std::max<long long>(1, (lag_items + per_stage - 1) / per_stage)));
+    const long long items = per_stage * p.units;
+    if (items > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
+    k1_fused<D, G><<<static_cast<unsigned>(items), kQThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <typename T, int D>
 cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
+    if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && k1_fused_on()) {
+        const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
+        return g == 1 ? launch_k1_fused<D, 1>(p, s) : launch_k1_fused<D, 2>(p, s);
+    }
     if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && !k1_alt(p)) {
         const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
         constexpr int smem = kBlockQ * D * 2;
