@@ -48,6 +48,10 @@
 #include <string>
 #include <vector>
 
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
+
 #include "../sageattn_b200.h"
 #include "quant.hpp"
 #include "tensor.hpp"
@@ -156,6 +160,35 @@ inline std::vector<int> devices_for_call() {
     return ids;
 }
 
+// The returned O.  Tensor4f's std::vector zero-fills its storage on the calling thread, and
+// for a large tensor that fill is dominated by 4 KB page faults (about a fifth of a second
+// per GB); on Linux the storage is reserved first and advised onto transparent huge pages,
+// then filled.  SAB_DROPIN_THP=0 skips the advice.
+inline Tensor4f alloc_output(int b, int h, int n, int d) {
+    Tensor4f t;
+    if (b < 1 || h < 1 || n < 1 || d < 1) throw std::invalid_argument("tensor dimensions must be positive");
+    t.batch = b;
+    t.heads = h;
+    t.tokens = n;
+    t.head_dim = d;
+    const size_t count = size_t(b) * size_t(h) * size_t(n) * size_t(d);
+#if defined(__linux__) && defined(MADV_HUGEPAGE)
+    static const bool thp = [] {
+        const char* e = std::getenv("SAB_DROPIN_THP");
+        return !(e && e[0] == '0');
+    }();
+    constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+    if (thp && count * sizeof(float) >= 16 * kHuge) {
+        t.data.reserve(count);
+        const uintptr_t a = (reinterpret_cast<uintptr_t>(t.data.data()) + kHuge - 1) & ~(kHuge - 1);
+        const uintptr_t e = reinterpret_cast<uintptr_t>(t.data.data() + count) & ~(kHuge - 1);
+        if (e > a) (void)madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // advice only
+    }
+#endif
+    t.data.resize(count);
+    return t;
+}
+
 inline void validate_input(const AttentionInput& in, const char* what) {
     if (!in.q.same_shape(in.k) || !in.q.same_shape(in.v))
         throw std::invalid_argument(std::string(what) + ": Q, K, V shapes differ");
@@ -196,7 +229,7 @@ inline Tensor4f sage_attention(const AttentionInput& in, const KernelConfig& con
     // attention.hpp:479: the static-scale counters exist only on the INT8 P~V path.
     SageDiagnostics* diag = options.diagnostics;
     d.measure_static_scale = (diag && diag->measure_static_scale && d.pv_path == SAB_PV_PATH_INT8) ? 1 : 0;
-    Tensor4f out(in.q.batch, in.q.heads, in.q.tokens, in.q.head_dim);
+    Tensor4f out = b200::alloc_output(in.q.batch, in.q.heads, in.q.tokens, in.q.head_dim);
     const std::vector<int> devs = b200::devices_for_call();
     uint64_t counts[3] = {0, 0, 0};
     b200::throw_status(sab_attention_fwd_host_diag(&d, in.q.data.data(), in.k.data.data(), in.v.data.data(),

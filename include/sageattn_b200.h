@@ -104,8 +104,9 @@ typedef struct sab_ws_layout {
     uint64_t partials;  /* float [units][n_partials][head_dim] mean tree partial sums  */
     uint64_t v16;       /* fp16  [units][tokens][head_dim]  V on the fp16 grid (F32 in)*/
     uint64_t status;    /* int32 device status word, two int32 K2 scheduler counters,
-                           then one int32 counter per unit (K1's mean tree); all zero
-                           between calls                                              */
+                           then three int32 counters per unit (K1's mean tree; the
+                           opt-in single-launch K1's mean-ready flags and K-chunk
+                           counts) and its ticket counter; all zero between calls     */
     uint64_t total;     /* workspace bytes                                            */
     int32_t n_partials; /* subtree sums per unit of the pairwise mean tree            */
     int32_t tree_depth; /* depth of the 4..9-token leaf level (quant.hpp:203-213)     */
