@@ -1101,11 +1101,10 @@ bool k1_fused_on() {
 template <int D, int G>
 cudaError_t launch_k1_fused(PrepassParams p, cudaStream_t s) {
     constexpr int smem = kBlockQ * D * 2;
-    static int resident = 0;  // CTAs of k1_fused resident on the device at once
-    cudaError_t e;
+    static int resident = 0;  // CTAs of k1_fused resident on a (B200) device at once
+    cudaError_t e = cudaFuncSetAttribute(k1_fused<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
     if (resident == 0) {
-        if ((e = cudaFuncSetAttribute(k1_fused<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
-            return e;
         int dev = 0, sms = 0, per_sm = 0;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
             (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess ||
