@@ -45,9 +45,17 @@ int tree_depth(int n) {
     return depth;
 }
 
+// Leaves of the mean tree summed per mean-partial CTA: any power of two keeps the tree
+// (the CTA sums an aligned perfect subtree, mean_top the perfect tree above).  32 by default;
+// SAB_K1_NODES (4, 8, 16 or 32) overrides it for tuning.
 int nodes_per_cta(int depth) {
+    static const int cap = [] {
+        const char* e = std::getenv("SAB_K1_NODES");
+        const int v = e ? std::atoi(e) : 32;
+        return (v == 4 || v == 8 || v == 16) ? v : 32;
+    }();
     const int nodes = 1 << depth;
-    return nodes < 32 ? nodes : 32;
+    return nodes < cap ? nodes : cap;
 }
 
 namespace {

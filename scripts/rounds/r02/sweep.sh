@@ -13,6 +13,6 @@ done; done; done
 for w in C2 C3 C5; do timeout 400 python bench.py --workload $w $B > gpurun_out/${T}_bench_$w.json 2>&1; done
 for sh in 8 4 2; do timeout 200 python bench.py --workload C2 --shard-of $sh $B > gpurun_out/${T}_bench_C2_shard$sh.json 2>&1; done
 for v in T VB VT; do timeout 300 python bench.py --workload C2 --variant $v $B > gpurun_out/${T}_bench_${v}_C2.json 2>&1; done
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${T}_launches_C2.csv python bench.py --workload C2 --steps 3 --warmup 1 --e2e-steps 1 $B > /dev/null 2>&1
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k1_|k2_" -c 40 --csv --log-file gpurun_out/${T}_launches_C2.csv python bench.py --workload C2 --steps 3 --warmup 1 --e2e-steps 1 $B > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k2_attention -s 2 -c 1 -o gpurun_out/${T}_k2_C4-128-16384-nc python bench.py --steps 2 --warmup 1 --e2e-steps 1 $B > /dev/null 2>&1
 ls gpurun_out | grep ${T}_ | wc -l
