@@ -31,6 +31,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -47,12 +48,12 @@ int tree_depth(int n) {
 
 // Leaves of the mean tree summed per mean-partial CTA: any power of two keeps the tree
 // (the CTA sums an aligned perfect subtree, mean_top the perfect tree above).  32 by default;
-// SAB_K1_NODES (4, 8, 16 or 32) overrides it for tuning.
+// SAB_K1_NODES (4, 8, 16, 32 or 64) overrides it for tuning.
 int nodes_per_cta(int depth) {
     static const int cap = [] {
         const char* e = std::getenv("SAB_K1_NODES");
         const int v = e ? std::atoi(e) : 32;
-        return (v == 4 || v == 8 || v == 16) ? v : 32;
+        return (v == 4 || v == 8 || v == 16 || v == 64) ? v : 32;
     }();
     const int nodes = 1 << depth;
     return nodes < cap ? nodes : cap;
@@ -811,8 +812,11 @@ __device__ __forceinline__ void q_chunk_fast(const PrepassParams& p, int unit, i
 #ifndef SAB_K1_MINB
 #define SAB_K1_MINB 4  // <= 64 registers: more Q-chunk CTAs in flight (C2 K1 78 -> 68 us)
 #endif
+#ifndef SAB_K1_MINB_G
+#define SAB_K1_MINB_G SAB_K1_MINB  // CTAs per SM bound when a thread group sums G >= 2 nodes
+#endif
 template <int D, int G>
-__global__ void __launch_bounds__(kQThreads, SAB_K1_MINB) k1_mean_and_q(PrepassParams p) {
+__global__ void __launch_bounds__(kQThreads, G >= 2 ? SAB_K1_MINB_G : SAB_K1_MINB) k1_mean_and_q(PrepassParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     griddep_launch_dependents();  // k1_k_fast may be scheduled behind this grid's last wave
     if (static_cast<int>(blockIdx.x) < p.n_partials) mean_partial<__half, D, G>(p, blockIdx.y, blockIdx.x);
@@ -1109,9 +1113,10 @@ bool k1_fused_on() {
 template <int D, int G>
 cudaError_t launch_k1_fused(PrepassParams p, cudaStream_t s) {
     constexpr int smem = kBlockQ * D * 2;
-    static int resident = 0;  // CTAs of k1_fused resident on a (B200) device at once
+    static std::atomic<int> resident_cache{0};  // CTAs of k1_fused resident on a (B200) device at once
     cudaError_t e = cudaFuncSetAttribute(k1_fused<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    int resident = resident_cache.load(std::memory_order_relaxed);
     if (resident == 0) {
         int dev = 0, sms = 0, per_sm = 0;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
@@ -1120,6 +1125,7 @@ cudaError_t launch_k1_fused(PrepassParams p, cudaStream_t s) {
                 cudaSuccess)
             return e;
         resident = std::max(1, sms * per_sm);
+        resident_cache.store(resident, std::memory_order_relaxed);
     }
     static const int pct = [] {
         const char* e = std::getenv("SAB_K1_LAG_PCT");
@@ -1140,7 +1146,7 @@ cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
     if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && k1_fused_on()) {
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
-        return g == 1 ? launch_k1_fused<D, 1>(p, s) : launch_k1_fused<D, 2>(p, s);
+        return g == 1 ? launch_k1_fused<D, 1>(p, s) : g == 2 ? launch_k1_fused<D, 2>(p, s) : launch_k1_fused<D, 4>(p, s);
     }
     if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && !k1_alt(p)) {
         const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
@@ -1150,9 +1156,12 @@ cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
         if (g == 1) {
             e = cudaFuncSetAttribute(k1_mean_and_q<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e == cudaSuccess) k1_mean_and_q<D, 1><<<dim3(p.n_partials + ntq, p.units), kQThreads, smem, s>>>(p);
-        } else {
+        } else if (g == 2) {
             e = cudaFuncSetAttribute(k1_mean_and_q<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e == cudaSuccess) k1_mean_and_q<D, 2><<<dim3(p.n_partials + ntq, p.units), kQThreads, smem, s>>>(p);
+        } else {
+            e = cudaFuncSetAttribute(k1_mean_and_q<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess) k1_mean_and_q<D, 4><<<dim3(p.n_partials + ntq, p.units), kQThreads, smem, s>>>(p);
         }
         if (e != cudaSuccess) return e;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1163,9 +1172,10 @@ cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     if (p.smooth) {
         const dim3 grid(p.n_partials, p.units);
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
-        switch (g) {  // nodes_per_cta() <= 32 -> at most 2 nodes per thread group
+        switch (g) {  // nodes_per_cta() <= 64 -> at most 4 nodes per thread group
             case 1: k1_mean_partials<T, D, 1><<<grid, kThreads, 0, s>>>(p); break;
             case 2: k1_mean_partials<T, D, 2><<<grid, kThreads, 0, s>>>(p); break;
+            case 4: k1_mean_partials<T, D, 4><<<grid, kThreads, 0, s>>>(p); break;
             default: return cudaErrorInvalidValue;
         }
         cudaError_t e = cudaGetLastError();
