@@ -943,13 +943,14 @@ __global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
     k_chunk_fast<D, false>(p, blockIdx.y, blockIdx.x, smem);
 }
 
-// ---- fp16, per-block path in ONE launch (opt-in experiment, SAB_K1_FUSED=1).  Each CTA
-// takes a ticket (atomic counter) and runs the work item of that ticket; items are ordered in stages, stage s = [mean partials of unit s][Q chunks of unit
-// s][K chunks of unit s - lag], so a K chunk waits (per-unit flag) only on CTAs with lower
-// tickets -- already running, so no deadlock -- and re-reads its K rows from L2 a few
-// units after the mean partials read them (lag ~ 1.5 resident waves of items): K comes
-// from DRAM once instead of twice, and there is no grid-wide dependency between K's mean
-// and its quantization.
+// ---- fp16, per-block path in ONE launch (opt-in experiment, SAB_K1_FUSED=1; measured
+// 1.1-1.35x slower than the two launches, profiles/r02_k1_fused_ab.txt).  Each CTA takes a
+// ticket (atomic counter) and runs the work item of that ticket.  Items are ordered in
+// stages, stage s = [mean partials of unit s][Q chunks of unit s][K chunks of unit s - lag],
+// so a K chunk waits (per-unit flag) only on CTAs with lower tickets -- already running, so
+// no deadlock -- and re-reads its K rows from L2 a few units after the mean partials read
+// them (lag ~ 1.5 resident waves of items): K comes from DRAM once instead of twice, and
+// there is no grid-wide dependency between K's mean and its quantization.
 template <int D, int G>
 __global__ void __launch_bounds__(kQThreads, SAB_K1_MINB) k1_fused(PrepassParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
