@@ -317,10 +317,10 @@ __device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, i
         float* dst = p.partials + (static_cast<size_t>(unit) * p.n_partials + chunk) * D + cv * 8;
 #pragma unroll
         for (int i = 0; i < 8; ++i) dst[i] = red[0][cv * 8 + i];
+        __threadfence();  // the writers publish the partial before the CTA's counter increment
     }
     // The last CTA of the unit to finish sums the top of the tree (no second launch).
     __shared__ int s_last;
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         s_last = atomicAdd(p.counters + unit, 1) == p.n_partials - 1;
