@@ -943,6 +943,18 @@ __global__ void __launch_bounds__(kQThreads) k1_k_fast(PrepassParams p) {
     k_chunk_fast<D, false>(p, blockIdx.y, blockIdx.x, smem);
 }
 
+// Q chunks in their own grid (SAB_K1_SPLITQ=1 experiment: k1_mean_partials -> k1_q_only ->
+// k1_k_fast, the Q chunks free of the partial path's register cap).  Q needs no mean(K); the
+// last CTA waits for the mean-partials grid before exiting, so this grid completes only after
+// it and k1_k_fast's wait on this grid covers mean(K).
+template <int D>
+__global__ void __launch_bounds__(kQThreads) k1_q_only(PrepassParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    griddep_launch_dependents();  // k1_k_fast's K loads may start behind this grid
+    q_chunk_fast<D>(p, blockIdx.y, blockIdx.x, smem);
+    if (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1) griddep_wait();
+}
+
 // ---- fp16, per-block path in ONE launch (opt-in experiment, SAB_K1_FUSED=1; measured
 // 1.1-1.35x slower than the two launches, profiles/r02_k1_fused_ab.txt).  Each CTA takes a
 // ticket (atomic counter) and runs the work item of that ticket.  Items are ordered in
@@ -1142,9 +1154,36 @@ cudaError_t launch_k1_fused(PrepassParams p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+bool k1_splitq_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("SAB_K1_SPLITQ");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 template <typename T, int D>
 cudaError_t launch_qk(const PrepassParams& p, cudaStream_t s) {
     constexpr int NG = kThreads / (D / 8);
+    if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && k1_splitq_on()) {
+        const int ntq = (p.n + kBlockQ - 1) / kBlockQ;
+        constexpr int smem = kBlockQ * D * 2;
+        const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
+        const dim3 grid(p.n_partials, p.units);
+        switch (g) {
+            case 1: k1_mean_partials<__half, D, 1><<<grid, kThreads, 0, s>>>(p); break;
+            case 2: k1_mean_partials<__half, D, 2><<<grid, kThreads, 0, s>>>(p); break;
+            case 4: k1_mean_partials<__half, D, 4><<<grid, kThreads, 0, s>>>(p); break;
+            default: return cudaErrorInvalidValue;
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if ((e = cudaFuncSetAttribute(k1_q_only<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess ||
+            (e = launch_pdl(k1_q_only<D>, dim3(ntq, p.units), dim3(kQThreads), smem, s, p)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k1_k_fast<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
+            return e;
+        return launch_pdl(k1_k_fast<D>, dim3(ntq, p.units), dim3(kQThreads), smem, s, p);
+    }
     if (std::is_same<T, __half>::value && p.smooth && !p.per_token && !p.rope && k1_fused_on()) {
         const int g = p.nodes_per_cta >= NG ? p.nodes_per_cta / NG : 1;
         return g == 1 ? launch_k1_fused<D, 1>(p, s) : g == 2 ? launch_k1_fused<D, 2>(p, s) : launch_k1_fused<D, 4>(p, s);
