@@ -338,8 +338,11 @@ __device__ __forceinline__ void mean_partial(const PrepassParams& p, int unit, i
     }
 }
 
+#ifndef SAB_K1_PART_MINB
+#define SAB_K1_PART_MINB 1  // CTAs per SM bound of k1_mean_partials (tuning)
+#endif
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads) k1_mean_partials(PrepassParams p) {
+__global__ void __launch_bounds__(kThreads, SAB_K1_PART_MINB) k1_mean_partials(PrepassParams p) {
     griddep_launch_dependents();  // k1_quantize's input loads may start behind this grid
     mean_partial<T, D, G>(p, blockIdx.y, blockIdx.x);
 }
